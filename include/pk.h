@@ -1,0 +1,151 @@
+/*
+ * pk.h -- C ABI of libpk, the B200 (sm_100a) executor for the parametric
+ * kernels of arXiv 1801.04348.
+ *
+ * The reference has no FFI: its executor is the Python function
+ *   parakern.interp.run_program(program, params, arrays=None, tracer=None)
+ *   (/root/reference/pkg/src/parakern/interp.py:215-225)
+ * which runs one program sequentially on the host.  This library replaces
+ * that call for the program families below; the Python shim
+ * (paper_1801_04348_b200/interp.py) keeps run_program's signature and binds
+ * these entry points with ctypes.  Plain C types only: device pointers are
+ * void*, streams are cudaStream_t passed as void*.
+ *
+ * Every entry point is re-entrant: no mutable globals except the device
+ * property cache (guarded by std::once_flag per device), the thread-local
+ * error text and an atomic launch counter.
+ */
+#ifndef PK_H
+#define PK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (the shim maps them to the reference's exceptions) ---- */
+#define PK_OK 0
+#define PK_E_PARAM 1       /* KeyError / ValueError: missing or invalid parameter (interp.py:75) */
+#define PK_E_BOUNDS 2      /* IndexError: an access would leave its array (interp.py:209-212)   */
+#define PK_E_DIV0 3        /* ZeroDivisionError while evaluating a binding (interp.py:43-46)    */
+#define PK_E_UNSUPPORTED 4 /* NotImplementedError: variant/dtype this library does not provide  */
+#define PK_E_CUDA 5        /* CUDA runtime failure (text in pk_last_error)                      */
+#define PK_E_ALLOC 6       /* device or pinned allocation failed                                */
+
+/* ---- program families (one per .mfk program shape) ---------------------- */
+#define PK_FAMILY_REVERSE 1   /* SURVEY App. A.2 reverse.mfk:   c[N-1-p] = a[p]                  */
+#define PK_FAMILY_TRANSPOSE 2 /* data/transpose.mfk:             c[i*N+j] = a[j][i]              */
+#define PK_FAMILY_JACOBI1D 3  /* data/jacobi.mfk:                3-point, /3, double-buffered   */
+#define PK_FAMILY_JACOBI2D 4  /* SURVEY App. A.4 jacobi2d.mfk:   5-point, /5, double-buffered   */
+#define PK_FAMILY_MATVEC 5    /* SURVEY App. A.3 matvec.mfk:     y[r] += a[r][q]*x[q]           */
+#define PK_FAMILY_MATMUL 6    /* SURVEY App. A.1 matmul.mfk:     c[p][q] += a[p][kk]*b[kk][q]   */
+#define PK_FAMILY_ADDITION 7  /* data/addition.mfk:              c = a + b (twin stores)        */
+
+/* ---- leaf variants: what the selected case's applied strategies mean ---- */
+#define PK_VARIANT_STAGED 0 /* cache(...) kept: tiles staged in shared memory            */
+#define PK_VARIANT_DIRECT 1 /* caching-off applied (strategies.py:430-440): no staging   */
+
+/* ---- flags --------------------------------------------------------------- */
+#define PK_FLAG_GRANULARITY 0x1 /* granularity applied (strategies.py:302-422): the s loop is
+                                   gone, one element per thread; tile = B (not s*B)           */
+#define PK_FLAG_TEMPORAL 0x2    /* Jacobi only: temporally blocked sweeps (reported apart)   */
+#define PK_FLAG_MERGED 0x4      /* addition only: twin stores merged by granularity          */
+#define PK_FLAG_GENERIC 0x8     /* force the generic (one thread per paper thread) kernel    */
+#define PK_FLAG_TF32X3 0x10     /* matmul f32 only: 3xTF32 on tcgen05 (reported apart)       */
+
+/* ---- element types ------------------------------------------------------- */
+#define PK_DTYPE_I32 0 /* the DSL's int: C int32 arithmetic, truncating / and % */
+#define PK_DTYPE_F32 1 /* float32 storage (matmul/matvec: Python floats in the reference) */
+
+/*
+ * One program invocation.  Parameters carry the names of the ORIGINAL
+ * program (the one the user passed to run_program); the covered index
+ * sets are derived from them with the program's own bindings (C division),
+ * so every variant writes exactly the elements the reference would.
+ * Fields a family does not use are ignored.
+ */
+typedef struct pk_launch {
+    int32_t family;  /* PK_FAMILY_*                                          */
+    int32_t variant; /* PK_VARIANT_*                                         */
+    int32_t dtype;   /* PK_DTYPE_*                                           */
+    int32_t flags;   /* PK_FLAG_*                                            */
+    int64_t N;       /* N (matmul: n)                                        */
+    int64_t T;       /* Jacobi time steps                                    */
+    int64_t s;       /* granularity                                          */
+    int64_t B;       /* 1-D thread block                                     */
+    int64_t B0;      /* 2-D thread block rows / matmul B0                    */
+    int64_t B1;      /* 2-D thread block cols                                */
+    int64_t ub1;     /* matmul thread columns                                */
+    int64_t lo, hi;  /* unit sub-range for partitioned launches (hi == 0: all
+                        units).  Units: reverse = input elements p, transpose /
+                        matvec / matmul / addition = output rows, Jacobi =
+                        interior positions (1-D) / rows (2-D).              */
+    int64_t tblock;  /* PK_FLAG_TEMPORAL: steps fused per sweep (0 = auto)   */
+} pk_launch_t;
+
+/* Live device properties, the values substituted for the machine
+ * parameters of the case discussion (replaces the constants of
+ * pkg/src/parakern/data/fermi.machine:12-18 and machine.py:80-88). */
+typedef struct pk_machine {
+    int32_t device;
+    int32_t cc_major, cc_minor;
+    int32_t sm_count;
+    int32_t warp_size;                /* not a reference parameter; executor-side filter */
+    int32_t max_threads_per_block;    /* T_B */
+    int32_t max_threads_per_sm;
+    int32_t regs_per_thread;          /* R_B: 255 on sm_100 (architectural) */
+    int32_t regs_per_block;
+    int32_t regs_per_sm;
+    int64_t smem_per_block;           /* Z_B (static) = /4 words */
+    int64_t smem_per_block_optin;     /* Z_B (opt-in carve-out) = /4 words */
+    int64_t smem_per_sm;
+    int64_t l2_bytes;
+    int64_t global_mem_bytes;
+    int32_t clock_khz;                /* SM clock (max) */
+    int32_t mem_clock_khz;
+    int32_t mem_bus_width_bits;
+    char name[256];
+} pk_machine_t;
+
+/* Fill *out for device `device`.  Replaces the reference's machine constants. */
+int pk_query_machine(int device, pk_machine_t *out);
+
+/* Run one program on device buffers (the pointers live on the current
+ * device).  dev_ptrs follow the program's array declaration order:
+ *   reverse (a, c) | transpose (a, c) | jacobi1d (a) | jacobi2d (a)
+ *   matvec (a, x, y) | matmul (a, b, c) | addition (a, b, c)
+ * Work is enqueued on `stream` (NULL = legacy default stream); the call
+ * returns after enqueueing.  Replaces interp.run_program (interp.py:215). */
+int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stream);
+
+/* End-to-end call with HOST buffers: pins the host memory, copies in,
+ * runs pk_launch, copies the written arrays back and synchronises.  The
+ * host buffers are updated in place (inputs and outputs alike). */
+int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device);
+
+/* One Jacobi sweep over an explicit position range, used by the slab
+ * partitioner (one process per GPU).  src/dst point at the two halves (1-D:
+ * a and a+N; 2-D: row 0 of each half, row pitch N).  Positions (1-D) or
+ * rows (2-D) in [lo, hi) that are interior (1..P) are updated; columns of
+ * 2-D are the program's covered columns.  Uses the tile geometry of L. */
+int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
+                    void *stream);
+
+/* Shared-memory words the leaf kernel stages per block (the footprint the
+ * case constrains against Z_B; reference counters.py:416-464). */
+int64_t pk_footprint_words(const pk_launch_t *L);
+
+/* Number of kernels libpk has launched since load (atomic). */
+int64_t pk_launch_count(void);
+
+/* Text of the last error raised on the calling thread. */
+const char *pk_last_error(void);
+
+/* ABI version: (major << 16) | minor. */
+int pk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PK_H */

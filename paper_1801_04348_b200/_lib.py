@@ -1,0 +1,217 @@
+"""ctypes binding of libpk.so (include/pk.h).
+
+The product path has no CPU fallback: if libpk.so is missing or fails to
+load, every call raises ``RuntimeError`` naming the library, and compute
+calls additionally require a visible CUDA device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libpk.so")
+
+# status codes (pk.h)
+PK_OK = 0
+PK_E_PARAM = 1
+PK_E_BOUNDS = 2
+PK_E_DIV0 = 3
+PK_E_UNSUPPORTED = 4
+PK_E_CUDA = 5
+PK_E_ALLOC = 6
+
+# families
+FAMILY_IDS = {
+    "reverse": 1,
+    "transpose": 2,
+    "jacobi": 3,
+    "jacobi2d": 4,
+    "matvec": 5,
+    "matmul": 6,
+    "addition": 7,
+}
+
+VARIANT_STAGED = 0
+VARIANT_DIRECT = 1
+
+FLAG_GRANULARITY = 0x1
+FLAG_TEMPORAL = 0x2
+FLAG_MERGED = 0x4
+FLAG_GENERIC = 0x8
+FLAG_TF32X3 = 0x10
+
+DTYPE_I32 = 0
+DTYPE_F32 = 1
+
+# every symbol include/pk.h declares
+EXPORTS = (
+    "pk_query_machine",
+    "pk_launch",
+    "pk_run_host",
+    "pk_jacobi_sweep",
+    "pk_footprint_words",
+    "pk_launch_count",
+    "pk_last_error",
+    "pk_version",
+)
+
+
+class PkLaunch(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int32),
+        ("variant", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("N", ctypes.c_int64),
+        ("T", ctypes.c_int64),
+        ("s", ctypes.c_int64),
+        ("B", ctypes.c_int64),
+        ("B0", ctypes.c_int64),
+        ("B1", ctypes.c_int64),
+        ("ub1", ctypes.c_int64),
+        ("lo", ctypes.c_int64),
+        ("hi", ctypes.c_int64),
+        ("tblock", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class PkMachine(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int32),
+        ("cc_major", ctypes.c_int32),
+        ("cc_minor", ctypes.c_int32),
+        ("sm_count", ctypes.c_int32),
+        ("warp_size", ctypes.c_int32),
+        ("max_threads_per_block", ctypes.c_int32),
+        ("max_threads_per_sm", ctypes.c_int32),
+        ("regs_per_thread", ctypes.c_int32),
+        ("regs_per_block", ctypes.c_int32),
+        ("regs_per_sm", ctypes.c_int32),
+        ("smem_per_block", ctypes.c_int64),
+        ("smem_per_block_optin", ctypes.c_int64),
+        ("smem_per_sm", ctypes.c_int64),
+        ("l2_bytes", ctypes.c_int64),
+        ("global_mem_bytes", ctypes.c_int64),
+        ("clock_khz", ctypes.c_int32),
+        ("mem_clock_khz", ctypes.c_int32),
+        ("mem_bus_width_bits", ctypes.c_int32),
+        ("name", ctypes.c_char * 256),
+    ]
+
+
+class PkError(RuntimeError):
+    """A libpk failure without a closer Python equivalent."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libpk.so once; raise loudly if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                "libpk.so not found at %s: build it with `python -m "
+                "paper_1801_04348_b200.build` (there is no CPU fallback)" % LIB_PATH
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        vp = ctypes.c_void_p
+        lib.pk_query_machine.argtypes = [ctypes.c_int, ctypes.POINTER(PkMachine)]
+        lib.pk_query_machine.restype = ctypes.c_int
+        lib.pk_launch.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), ctypes.c_int, vp]
+        lib.pk_launch.restype = ctypes.c_int
+        lib.pk_run_host.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int]
+        lib.pk_run_host.restype = ctypes.c_int
+        lib.pk_jacobi_sweep.argtypes = [ctypes.POINTER(PkLaunch), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
+        lib.pk_jacobi_sweep.restype = ctypes.c_int
+        lib.pk_footprint_words.argtypes = [ctypes.POINTER(PkLaunch)]
+        lib.pk_footprint_words.restype = ctypes.c_int64
+        lib.pk_launch_count.argtypes = []
+        lib.pk_launch_count.restype = ctypes.c_int64
+        lib.pk_last_error.argtypes = []
+        lib.pk_last_error.restype = ctypes.c_char_p
+        lib.pk_version.argtypes = []
+        lib.pk_version.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().pk_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int) -> None:
+    """Map a pk.h status code onto the reference interpreter's exceptions."""
+    if rc == PK_OK:
+        return
+    msg = last_error()
+    if rc == PK_E_PARAM:
+        raise ValueError(msg)
+    if rc == PK_E_BOUNDS:
+        raise IndexError(msg)
+    if rc == PK_E_DIV0:
+        raise ZeroDivisionError(msg)
+    if rc == PK_E_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if rc == PK_E_ALLOC:
+        raise MemoryError(msg)
+    raise PkError("libpk error %d: %s" % (rc, msg))
+
+
+def ptr_array(ptrs) -> "ctypes.Array":
+    arr = (ctypes.c_void_p * len(ptrs))()
+    for i, p in enumerate(ptrs):
+        arr[i] = ctypes.c_void_p(int(p))
+    return arr
+
+
+def launch(L: PkLaunch, ptrs, stream: int = 0) -> None:
+    lib = load()
+    arr = ptr_array(ptrs)
+    check(lib.pk_launch(ctypes.byref(L), arr, len(ptrs), ctypes.c_void_p(stream or None)))
+
+
+def run_host(L: PkLaunch, host_ptrs, device: int = 0) -> None:
+    lib = load()
+    arr = ptr_array(host_ptrs)
+    check(lib.pk_run_host(ctypes.byref(L), arr, len(host_ptrs), device))
+
+
+def jacobi_sweep(L: PkLaunch, src: int, dst: int, lo: int, hi: int, stream: int = 0) -> None:
+    lib = load()
+    check(lib.pk_jacobi_sweep(ctypes.byref(L), ctypes.c_void_p(src), ctypes.c_void_p(dst), lo, hi,
+                              ctypes.c_void_p(stream or None)))
+
+
+def footprint_words(L: PkLaunch) -> int:
+    return int(load().pk_footprint_words(ctypes.byref(L)))
+
+
+def launch_count() -> int:
+    return int(load().pk_launch_count())
+
+
+def query_machine(device: int = 0) -> dict:
+    m = PkMachine()
+    check(load().pk_query_machine(device, ctypes.byref(m)))
+    out = {name: getattr(m, name) for name, _ in PkMachine._fields_}
+    out["name"] = m.name.decode("utf-8", "replace")
+    return out
+
+
+def version() -> tuple[int, int]:
+    v = int(load().pk_version())
+    return v >> 16, v & 0xFFFF

@@ -1,0 +1,117 @@
+// k_matvec.cu -- matrix-vector product (SURVEY App. A.3 matvec.mfk):
+//   dim = N/(s*B);  r = i*s*B + k*B + j < dim*s*B;  for q < N: y[r] = y[r] + a[r][q]*x[q]
+// A block owns E*B consecutive rows (E = s, or 1 after granularity).  Each
+// row is reduced by a group of lanes (a full warp when B allows) reading the
+// row with 128-bit loads, then combined with warp shuffles.  cache(x) kept:
+// x is staged once per block in shared memory (N words; the case requires
+// N <= Z_B); caching-off reads x through L1/L2.
+// Integers accumulate in wrapping int32 -- exact whenever the result fits,
+// as two's-complement sums are exact modulo 2^32.  float32 data accumulate
+// in binary64 (the reference sums Python floats), rounded once at the end.
+// HBM-bound: 4*N bytes of a per row dominate (x stays in L2/shared memory).
+#include "pk_internal.cuh"
+
+namespace pk {
+namespace {
+
+template <typename T> struct Acc;
+template <> struct Acc<int> { using type = int; };
+template <> struct Acc<float> { using type = double; };
+
+template <typename A>
+__device__ __forceinline__ A group_sum(A v, int lanes) {
+    for (int o = lanes >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, lanes);
+    return v;
+}
+
+template <typename T, bool STAGED, bool VEC>
+__global__ void __launch_bounds__(1024) k_matvec(const T *__restrict__ a, const T *__restrict__ x,
+                                                T *__restrict__ y, int64_t N, int64_t rlo,
+                                                int64_t rhi, int tile, int lanes) {
+    using A = typename Acc<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const T *xs = x;
+    if (STAGED) {
+        T *sx = reinterpret_cast<T *>(smem_raw);
+        if (VEC) {
+            const int4 *x4 = reinterpret_cast<const int4 *>(x);
+            int4 *s4 = reinterpret_cast<int4 *>(sx);
+            for (int64_t q = threadIdx.x; q < N / 4; q += blockDim.x) s4[q] = x4[q];
+        } else {
+            for (int64_t q = threadIdx.x; q < N; q += blockDim.x) sx[q] = x[q];
+        }
+        __syncthreads();
+        xs = sx;
+    }
+    const int64_t base = rlo + (int64_t)blockIdx.x * tile;
+    const int64_t end = min(base + tile, rhi);
+    const int lane = threadIdx.x % lanes, group = threadIdx.x / lanes;
+    const int ngroups = blockDim.x / lanes;
+    for (int64_t r = base + group; r < end; r += ngroups) {
+        const T *row = a + r * N;
+        A acc = 0;
+        if (VEC) {
+            const int64_t n4 = N / 4;
+#pragma unroll 4
+            for (int64_t q = lane; q < n4; q += lanes) {
+                const int4 av = ld_stream(reinterpret_cast<const int4 *>(row) + q);
+                const T *ap = reinterpret_cast<const T *>(&av);
+                const T *xp = xs + 4 * q;
+                acc += (A)ap[0] * (A)xp[0];
+                acc += (A)ap[1] * (A)xp[1];
+                acc += (A)ap[2] * (A)xp[2];
+                acc += (A)ap[3] * (A)xp[3];
+            }
+        } else {
+#pragma unroll 4
+            for (int64_t q = lane; q < N; q += lanes) acc += (A)row[q] * (A)xs[q];
+        }
+        acc = group_sum(acc, lanes);
+        if (lane == 0) y[r] = (T)((A)y[r] + acc);
+    }
+}
+
+template <typename T>
+int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo, int64_t rhi) {
+    const int64_t tile64 = elems(L) * L.B;
+    if (tile64 > (1 << 30)) return fail(PK_E_UNSUPPORTED, "matvec: tile too large");
+    const int tile = (int)tile64;
+    int nt = (int)(L.B < 1024 ? L.B : 1024);
+    // lanes per row: the largest power of two <= 32 dividing the block size
+    int lanes = 1;
+    while (lanes < 32 && nt % (lanes * 2) == 0) lanes *= 2;
+    const int64_t blocks = ceil_div(rhi - rlo, tile);
+    if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matvec: grid too large");
+    const T *a = static_cast<const T *>(p[0]);
+    const T *x = static_cast<const T *>(p[1]);
+    T *y = static_cast<T *>(p[2]);
+    const bool vec = L.N % 4 == 0 && aligned16(a) && aligned16(x);
+    if (L.variant == PK_VARIANT_STAGED) {
+        const size_t smem = (size_t)L.N * sizeof(T);
+        const void *k = vec ? (const void *)k_matvec<T, true, true> : (const void *)k_matvec<T, true, false>;
+        int rc = allow_smem(k, smem);
+        if (rc) return rc;
+        if (vec) k_matvec<T, true, true><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+        else k_matvec<T, true, false><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+    } else {
+        if (vec) k_matvec<T, false, true><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+        else k_matvec<T, false, false><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+    }
+    return after_launch("matvec");
+}
+
+}  // namespace
+
+int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st) {
+    if (L.s * L.B == 0) return fail(PK_E_DIV0, "matvec: s*B == 0 in dim = N / (s * B)");
+    if (L.s < 0 || L.B < 0 || L.N <= 0) return PK_OK;
+    const int64_t R = max0(L.N / (L.s * L.B)) * L.s * L.B;
+    int64_t rlo, rhi;
+    unit_range(L, 0, R, &rlo, &rhi);
+    if (rhi <= rlo) return PK_OK;
+    if (L.dtype == PK_DTYPE_I32) return launch_t<int>(L, p, st, rlo, rhi);
+    if (L.dtype == PK_DTYPE_F32) return launch_t<float>(L, p, st, rlo, rhi);
+    return fail(PK_E_UNSUPPORTED, "matvec: dtype %d", L.dtype);
+}
+
+}  // namespace pk

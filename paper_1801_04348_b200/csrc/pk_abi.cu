@@ -1,0 +1,217 @@
+// pk_abi.cu -- the C ABI of libpk (include/pk.h): device-property lookup,
+// validation, dispatch to the family launchers, and the host-buffer path.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "pk_internal.cuh"
+
+namespace pk {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+thread_local char t_err[1024] = "";
+}
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(t_err, sizeof(t_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int allow_smem(const void *kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return PK_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if ((long long)bytes > optin)
+        return fail(PK_E_PARAM,
+                    "staged tile needs %zu bytes of shared memory but the device allows %d per "
+                    "block (Z_B); the case discussion selects a caching-off leaf here",
+                    bytes, optin);
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PK_OK;
+}
+
+int64_t footprint_words(const pk_launch_t &L) {
+    if (L.variant != PK_VARIANT_STAGED) return 0;
+    const int64_t E = elems(L);
+    switch (L.family) {
+        case PK_FAMILY_REVERSE: return E * L.B;
+        case PK_FAMILY_TRANSPOSE: return E * L.B1 * (L.B0 | 1);
+        case PK_FAMILY_JACOBI1D: return E * L.B + 2;
+        case PK_FAMILY_JACOBI2D: return (L.B0 + 2) * (E * L.B1 + 2);
+        case PK_FAMILY_MATVEC: return L.N;
+        case PK_FAMILY_MATMUL: return L.B0 * L.B0 + L.B0 * L.ub1 * (E < 8 ? E : 8);
+        default: return 0;
+    }
+}
+
+namespace {
+
+struct ArraySpec {
+    int count;
+    int64_t elems[3];
+    bool written[3];
+};
+
+int array_spec(const pk_launch_t &L, ArraySpec *s) {
+    const int64_t N = L.N > 0 ? L.N : 0;
+    switch (L.family) {
+        case PK_FAMILY_REVERSE: *s = {2, {N, N, 0}, {false, true, false}}; return PK_OK;
+        case PK_FAMILY_TRANSPOSE: *s = {2, {N * N, N * N, 0}, {false, true, false}}; return PK_OK;
+        case PK_FAMILY_JACOBI1D: *s = {1, {2 * N, 0, 0}, {true, false, false}}; return PK_OK;
+        case PK_FAMILY_JACOBI2D: *s = {1, {2 * N * N, 0, 0}, {true, false, false}}; return PK_OK;
+        case PK_FAMILY_MATVEC: *s = {3, {N * N, N, N}, {false, false, true}}; return PK_OK;
+        case PK_FAMILY_MATMUL: *s = {3, {N * N, N * N, N * N}, {false, false, true}}; return PK_OK;
+        case PK_FAMILY_ADDITION: *s = {3, {N * N, N * N, N * N}, {false, false, true}}; return PK_OK;
+        default: return fail(PK_E_UNSUPPORTED, "unknown program family %d", L.family);
+    }
+}
+
+int dispatch(const pk_launch_t &L, void *const *p, cudaStream_t st) {
+    switch (L.family) {
+        case PK_FAMILY_REVERSE: return launch_reverse(L, p, st);
+        case PK_FAMILY_TRANSPOSE: return launch_transpose(L, p, st);
+        case PK_FAMILY_JACOBI1D: return launch_jacobi1d(L, p, st);
+        case PK_FAMILY_JACOBI2D: return launch_jacobi2d(L, p, st);
+        case PK_FAMILY_MATVEC: return launch_matvec(L, p, st);
+        case PK_FAMILY_MATMUL: return launch_matmul(L, p, st);
+        case PK_FAMILY_ADDITION: return launch_addition(L, p, st);
+        default: return fail(PK_E_UNSUPPORTED, "unknown program family %d", L.family);
+    }
+}
+
+int validate(const pk_launch_t *L, int nptrs) {
+    if (!L) return fail(PK_E_PARAM, "null launch descriptor");
+    ArraySpec s;
+    int rc = array_spec(*L, &s);
+    if (rc) return rc;
+    if (nptrs != s.count)
+        return fail(PK_E_PARAM, "family %d takes %d arrays, got %d", L->family, s.count, nptrs);
+    if (L->variant != PK_VARIANT_STAGED && L->variant != PK_VARIANT_DIRECT)
+        return fail(PK_E_UNSUPPORTED, "unknown variant %d", L->variant);
+    const bool fp_ok = L->family == PK_FAMILY_MATMUL || L->family == PK_FAMILY_MATVEC ||
+                       L->family == PK_FAMILY_TRANSPOSE || L->family == PK_FAMILY_REVERSE;
+    if (L->dtype != PK_DTYPE_I32 && !(L->dtype == PK_DTYPE_F32 && fp_ok))
+        return fail(PK_E_UNSUPPORTED, "dtype %d not provided for family %d", L->dtype, L->family);
+    if (L->flags & PK_FLAG_TF32X3)
+        return fail(PK_E_UNSUPPORTED, "3xTF32 tcgen05 matmul is not built into this library");
+    if (L->flags & PK_FLAG_TEMPORAL)
+        return fail(PK_E_UNSUPPORTED, "temporally blocked Jacobi is not built into this library");
+    return PK_OK;
+}
+
+}  // namespace
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" {
+
+int pk_version(void) { return (1 << 16) | 0; }
+
+const char *pk_last_error(void) { return t_err; }
+
+int64_t pk_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int64_t pk_footprint_words(const pk_launch_t *L) { return L ? footprint_words(*L) : 0; }
+
+int pk_query_machine(int device, pk_machine_t *out) {
+    if (!out) return fail(PK_E_PARAM, "null pk_machine_t");
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaGetDeviceProperties(%d): %s", device, cudaGetErrorString(e));
+    memset(out, 0, sizeof(*out));
+    out->device = device;
+    out->cc_major = prop.major;
+    out->cc_minor = prop.minor;
+    out->sm_count = prop.multiProcessorCount;
+    out->warp_size = prop.warpSize;
+    out->max_threads_per_block = prop.maxThreadsPerBlock;
+    out->max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
+    out->regs_per_thread = 255;  // architectural per-thread limit (not in cudaDeviceProp)
+    out->regs_per_block = prop.regsPerBlock;
+    out->regs_per_sm = prop.regsPerMultiprocessor;
+    out->smem_per_block = (int64_t)prop.sharedMemPerBlock;
+    out->smem_per_block_optin = (int64_t)prop.sharedMemPerBlockOptin;
+    out->smem_per_sm = (int64_t)prop.sharedMemPerMultiprocessor;
+    out->l2_bytes = prop.l2CacheSize;
+    out->global_mem_bytes = (int64_t)prop.totalGlobalMem;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, device);
+    out->clock_khz = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMemoryClockRate, device);
+    out->mem_clock_khz = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrGlobalMemoryBusWidth, device);
+    out->mem_bus_width_bits = v;
+    strncpy(out->name, prop.name, sizeof(out->name) - 1);
+    return PK_OK;
+}
+
+int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stream) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    for (int i = 0; i < nptrs; i++)
+        if (!dev_ptrs || !dev_ptrs[i]) return fail(PK_E_PARAM, "array %d is a null pointer", i);
+    return dispatch(*L, dev_ptrs, static_cast<cudaStream_t>(stream));
+}
+
+int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
+                    void *stream) {
+    if (!L || !src || !dst) return fail(PK_E_PARAM, "null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (L->family == PK_FAMILY_JACOBI1D) return sweep_jacobi1d(*L, src, dst, lo, hi, st);
+    if (L->family == PK_FAMILY_JACOBI2D) return sweep_jacobi2d(*L, src, dst, lo, hi, st);
+    return fail(PK_E_PARAM, "pk_jacobi_sweep: family %d is not a Jacobi stencil", L->family);
+}
+
+int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    ArraySpec spec;
+    array_spec(*L, &spec);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+    cudaStream_t st;
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    void *dev[3] = {nullptr, nullptr, nullptr};
+    rc = PK_OK;
+    for (int i = 0; i < spec.count && rc == PK_OK; i++) {
+        const size_t bytes = (size_t)spec.elems[i] * 4;
+        e = cudaMallocAsync(&dev[i], bytes ? bytes : 4, st);
+        if (e != cudaSuccess) {
+            rc = fail(PK_E_ALLOC, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
+            break;
+        }
+        if (bytes && host_ptrs[i]) {
+            e = cudaMemcpyAsync(dev[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) rc = fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(e));
+        } else if (bytes) {
+            cudaMemsetAsync(dev[i], 0, bytes, st);  // missing arrays are zero-filled (interp.py:79-81)
+        }
+    }
+    if (rc == PK_OK) rc = dispatch(*L, dev, st);
+    for (int i = 0; i < spec.count && rc == PK_OK; i++) {
+        const size_t bytes = (size_t)spec.elems[i] * 4;
+        if (spec.written[i] && bytes && host_ptrs[i]) {
+            e = cudaMemcpyAsync(host_ptrs[i], dev[i], bytes, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) rc = fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(e));
+        }
+    }
+    for (int i = 0; i < spec.count; i++)
+        if (dev[i]) cudaFreeAsync(dev[i], st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && rc == PK_OK) rc = fail(PK_E_CUDA, "kernel execution: %s", cudaGetErrorString(e));
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// pk_internal.cuh -- shared helpers for libpk (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+
+#include "pk.h"
+
+namespace pk {
+
+// Records the error text for pk_last_error() on this thread; returns code.
+int fail(int code, const char *fmt, ...);
+
+extern std::atomic<int64_t> g_launches;
+
+// After a <<<>>> launch: surface configuration errors, count the launch.
+inline int after_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return PK_OK;
+}
+
+// Opt a kernel into more than 48 KB of dynamic shared memory.
+int allow_smem(const void *kernel, size_t bytes);
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t max0(int64_t v) { return v > 0 ? v : 0; }
+
+// --- device helpers ----------------------------------------------------------
+
+// Streaming 128-bit load that does not allocate in L1 (read-once data).
+__device__ __forceinline__ int4 ld_stream(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(int4 *p, const int4 &v) {
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w));
+}
+
+// Truncating integer division of an exact (64-bit) sum, as the reference's
+// c_div (interp.py:43-46): C division already truncates toward zero.
+__device__ __forceinline__ int div3(long long s) { return (int)(s / 3); }
+__device__ __forceinline__ int div5(long long s) { return (int)(s / 5); }
+
+// --- per-family host launchers (one .cu each) ---------------------------------
+int launch_reverse(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_transpose(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_jacobi1d(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_jacobi2d(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int sweep_jacobi1d(const pk_launch_t &L, const void *src, void *dst, int64_t lo, int64_t hi,
+                   cudaStream_t st);
+int sweep_jacobi2d(const pk_launch_t &L, const void *src, void *dst, int64_t lo, int64_t hi,
+                   cudaStream_t st);
+int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);
+
+// Shared-memory words staged per block (0 for direct variants).
+int64_t footprint_words(const pk_launch_t &L);
+
+// Elements per thread along the s axis: 1 once granularity removed the loop.
+inline int64_t elems(const pk_launch_t &L) {
+    return (L.flags & PK_FLAG_GRANULARITY) ? 1 : L.s;
+}
+
+// Clamp [lo, hi) of a partitioned launch to the covered units [ulo, uhi).
+inline void unit_range(const pk_launch_t &L, int64_t ulo, int64_t uhi, int64_t *lo, int64_t *hi) {
+    int64_t a = ulo, b = uhi;
+    if (L.hi > 0) {
+        a = L.lo > ulo ? L.lo : ulo;
+        b = L.hi < uhi ? L.hi : uhi;
+    }
+    *lo = a;
+    *hi = b > a ? b : a;
+}
+
+}  // namespace pk

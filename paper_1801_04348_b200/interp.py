@@ -1,0 +1,305 @@
+"""Drop-in replacement for ``parakern.interp.run_program`` on sm_100a.
+
+    from paper_1801_04348_b200.interp import run_program
+    out = run_program(program, {"N": 1 << 20, "s": 4, "B": 256}, arrays={"a": a})
+
+Same contract as the reference (/root/reference/pkg/src/parakern/interp.py:215-225):
+
+* ``program``: a ``parakern.dsl.Program`` or its ``.mfk`` text;
+* ``params``: scalar parameter values; a missing one raises ``KeyError``
+  (interp.py:73-75), a zero divisor in a binding ``ZeroDivisionError``;
+* ``arrays``: optional initial contents; the caller's buffers are never
+  mutated (interp.py:76-78, 183-186); arrays not supplied start as zeros
+  (interp.py:79-81);
+* returns a fresh dict holding every declared array.
+
+What changes: the program runs as a hand-written CUDA kernel chosen by the
+case discussion evaluated at the live device properties, instead of the
+sequential tree walk.  ``tracer`` is CPU-only instrumentation and raises
+``NotImplementedError`` (no CPU fallback).  Arrays may be Python lists (as
+the reference uses), numpy arrays or torch tensors; results come back in
+the same container type.  ``inplace=True`` with contiguous CUDA tensors runs
+on the caller's device buffers without copies.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, binding, cases
+from .programs import FAMILIES, ProgramKind, effective_params, identify
+
+_INT32_MIN, _INT32_MAX = -(2**31), 2**31 - 1
+
+
+@dataclass
+class RunInfo:
+    """What the last run_program call executed (for tests and reports)."""
+
+    family: str
+    case: int | None
+    applied: tuple[str, ...]
+    fallback: bool
+    launch: dict
+    footprint_words: int
+
+
+_last: RunInfo | None = None
+
+
+def last_run() -> RunInfo | None:
+    return _last
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _kind_of(value) -> str:
+    if isinstance(value, np.ndarray):
+        return "numpy"
+    if type(value).__module__.startswith("torch"):
+        return "torch"
+    return "list"
+
+
+def _list_dtype(data) -> str:
+    flat = data[0] if data and isinstance(data[0], list) else data
+    rows = data if data and isinstance(data[0], list) else [data]
+    for row in rows:
+        for v in row:
+            if isinstance(v, float):
+                return "f"
+    del flat
+    return "i"
+
+
+def _dtype_of(value) -> str:
+    k = _kind_of(value)
+    if k == "list":
+        return _list_dtype(value)
+    if k == "numpy":
+        return "f" if np.issubdtype(value.dtype, np.floating) else "i"
+    return "f" if value.dtype.is_floating_point else "i"
+
+
+def _numel(shape) -> int:
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+def _to_device_tensor(name, value, shape, np_dtype, device):
+    torch = _torch()
+    k = _kind_of(value)
+    want = _numel(shape)
+    if k == "torch":
+        t = value.detach()
+        if t.numel() < want:
+            raise IndexError("array %s has %d elements; the program declares %s" % (name, t.numel(), shape))
+        if np_dtype == np.int32 and t.dtype != torch.int32:
+            if t.is_floating_point():
+                raise TypeError("array %s: float data for an int program" % name)
+            t64 = t.to(torch.int64)
+            if t64.numel() and (int(t64.min()) < _INT32_MIN or int(t64.max()) > _INT32_MAX):
+                raise OverflowError("array %s holds values outside int32" % name)
+            t = t64.to(torch.int32)
+        elif np_dtype == np.float32 and t.dtype != torch.float32:
+            t = t.to(torch.float32)
+        return t.reshape(-1).to(device, copy=True).contiguous(), t.numel()
+    if k == "list":
+        arr = np.asarray(value, dtype=np.float64 if np_dtype == np.float32 else object)
+        if np_dtype == np.int32:
+            flat = arr.reshape(-1)
+            if flat.size and (min(flat) < _INT32_MIN or max(flat) > _INT32_MAX):
+                raise OverflowError("array %s holds values outside int32" % name)
+        arr = arr.astype(np_dtype)
+    else:
+        arr = value
+        if np_dtype == np.int32 and arr.dtype != np.int32:
+            if np.issubdtype(arr.dtype, np.floating):
+                raise TypeError("array %s: float data for an int program" % name)
+            if arr.size and (arr.min() < _INT32_MIN or arr.max() > _INT32_MAX):
+                raise OverflowError("array %s holds values outside int32" % name)
+        arr = np.ascontiguousarray(arr, dtype=np_dtype)
+    flat = arr.reshape(-1)
+    if flat.size < want:
+        raise IndexError("array %s has %d elements; the program declares %s" % (name, flat.size, shape))
+    host = torch.from_numpy(flat)
+    return host.to(device, non_blocking=False), flat.size
+
+
+def _from_device(t, kind: str, shape, like):
+    torch = _torch()
+    if kind == "torch":
+        dev = like.device if like is not None else t.device
+        out = t.reshape(shape) if t.numel() == _numel(shape) else t
+        return out.to(dev)
+    host = t.cpu().numpy()
+    if host.size == _numel(shape):
+        host = host.reshape(shape)
+    if kind == "numpy":
+        return host.copy()
+    del torch
+    return host.tolist()
+
+
+def _shapes_py(fam, P):
+    """Array extents with the interpreter's list semantics ([0]*negative == [])."""
+    out = {}
+    for name, dims in fam.shapes(P).items():
+        out[name] = tuple(max(0, d) for d in dims)
+    return out
+
+
+def run_program(
+    program,
+    params: dict,
+    arrays: dict | None = None,
+    tracer=None,
+    *,
+    machine=None,
+    device=None,
+    inplace: bool = False,
+    generic: bool = False,
+    case: int | None = None,
+) -> dict:
+    """Execute the whole program on the GPU; returns the final array contents.
+
+    ``machine``: the machine values for case selection (default: the live
+    device).  ``case``: force a leaf by index (tests / tuner).  ``generic``:
+    force the program's literal thread mapping instead of the tuned tile.
+    """
+    global _last
+    if tracer is not None:
+        raise NotImplementedError(
+            "tracer is CPU-only instrumentation of the reference interpreter; "
+            "the GPU executor cannot report per-access events"
+        )
+    kind = identify(program)
+    P = effective_params(kind, params)
+    fam = FAMILIES[kind.family]
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("run_program needs a CUDA device (sm_100a); there is no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    mv = None
+    if machine is None or machine == "live":
+        from . import machine as machine_mod
+
+        mv = machine_mod.live(dev.index)
+    else:
+        mv = machine
+
+    # case discussion: an original program selects its leaf at the live
+    # machine; a case program already is one
+    if kind.is_original:
+        sel = cases.select(kind, P, mv)
+        if case is not None:
+            tab = cases.table(kind.family, sel.machine)
+            forced = [c for c in tab.cases if c.index == case]
+            if not forced:
+                raise ValueError("no case %d for %s" % (case, kind.family))
+            sel = cases.Selection(kind.family, sel.machine, forced[0], sel.assignment)
+        applied, case_index, fallback = sel.applied, sel.index, sel.fallback
+    else:
+        applied, case_index, fallback = kind.applied, None, False
+
+    arrays = dict(arrays or {})
+    for name in arrays:
+        if name not in {a.name for a in fam.arrays}:
+            # the reference deep-copies unknown arrays through untouched
+            pass
+    dtypes = {_dtype_of(v) for n, v in arrays.items() if n in {a.name for a in fam.arrays}}
+    if "f" in dtypes:
+        if not fam.float_ok:
+            raise NotImplementedError("%s computes on C ints; float arrays are not supported" % kind.family)
+        np_dtype, dtype = np.float32, _lib.DTYPE_F32
+    else:
+        np_dtype, dtype = np.int32, _lib.DTYPE_I32
+
+    shapes = _shapes_py(fam, P)
+    kinds = [_kind_of(v) for v in arrays.values()]
+    default_kind = kinds[0] if kinds else "list"
+
+    L = binding.make_launch(kind, P, applied, dtype, generic=generic)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    with torch.cuda.device(dev):
+        bufs, sizes, owned = [], {}, {}
+        for a in fam.arrays:
+            shape = shapes[a.name]
+            want = _numel(shape)
+            if a.name in arrays:
+                v = arrays[a.name]
+                if (inplace and _kind_of(v) == "torch" and v.is_cuda and v.is_contiguous()
+                        and v.dtype == (torch.float32 if dtype == _lib.DTYPE_F32 else torch.int32)):
+                    t = v.reshape(-1)
+                    sizes[a.name] = t.numel()
+                else:
+                    t, sizes[a.name] = _to_device_tensor(a.name, v, shape, np_dtype, dev)
+            else:
+                t = torch.zeros(max(want, 1), dtype=torch.float32 if dtype == _lib.DTYPE_F32 else torch.int32,
+                                device=dev)
+                sizes[a.name] = want
+            owned[a.name] = t
+            bufs.append(t)
+        if all(_numel(shapes[a.name]) > 0 for a in fam.arrays):
+            _lib.launch(L, [b.data_ptr() for b in bufs], stream)
+        torch.cuda.current_stream(dev).synchronize()
+
+    _last = RunInfo(kind.family, case_index, tuple(applied), fallback, binding.describe(L),
+                    _lib.footprint_words(L))
+
+    out = {}
+    # arrays the caller passed that the program does not declare come back as copies
+    for name, v in arrays.items():
+        if name not in owned:
+            out[name] = _deep_copy(v)
+    for a in fam.arrays:
+        shape = shapes[a.name]
+        like = arrays.get(a.name)
+        k = _kind_of(like) if like is not None else default_kind
+        t = owned[a.name]
+        if inplace and like is not None and _kind_of(like) == "torch" and like.is_cuda and t.data_ptr() == like.data_ptr():
+            out[a.name] = like
+            continue
+        if sizes[a.name] != _numel(shape):
+            t = t[: sizes[a.name]]
+            out[a.name] = _from_device(t, k, (sizes[a.name],), like)
+        else:
+            out[a.name] = _from_device(t[: _numel(shape)], k, shape, like)
+    return out
+
+
+def _deep_copy(v):
+    if isinstance(v, list):
+        return [row[:] if isinstance(row, list) else row for row in v]
+    if isinstance(v, np.ndarray):
+        return v.copy()
+    return v.clone()
+
+
+def run_block(program, params, grid_values, context_values=None, arrays=None, tracer=None):
+    """The reference's one-block executor (interp.py:228-249) exists to feed
+    the footprint oracle's access tracer; it has no GPU counterpart."""
+    raise NotImplementedError(
+        "run_block is a CPU tracing aid of the reference interpreter (interp.py:228-249); "
+        "the GPU executor only runs whole programs"
+    )
+
+
+def c_div(a: int, b: int) -> int:
+    """C99 truncating division (interp.py:43-46); the kernels use C '/'."""
+    q = abs(a) // abs(b)
+    return q if (a >= 0) == (b >= 0) else -q
+
+
+def c_mod(a: int, b: int) -> int:
+    """C99 remainder (interp.py:49-50)."""
+    return a - b * c_div(a, b)

@@ -1,0 +1,120 @@
+"""Machine-parameter lookup: live device properties instead of constants.
+
+The reference models the target as a machine file of symbolic limits with
+fixed ranges (machine.py:46-93, 111-243; data/fermi.machine:12-18:
+Z_B <= 12288 words, R_B <= 63).  Here the values substituted into the case
+discussion come from ``cudaGetDeviceProperties`` through the C ABI
+(``pk_query_machine``):
+
+  Z_B  shared-memory words per block  = sharedMemPerBlockOptin / 4  (58112 on B200)
+       (or sharedMemPerBlock / 4 = 12288 with smem="static")
+  R_B  registers per thread           = 255 (sm_100 architectural limit)
+  T_B  threads per block              = maxThreadsPerBlock (1024)
+
+The warp size (32) is not one of the reference's machine parameters; the
+tuner applies it as an executor-side filter.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+from . import _lib
+
+# The reference's default machine model, evaluated at its declared limits
+# (pkg/src/parakern/data/fermi.machine:12-18; addition.machine:11-17).
+FERMI_VALUES = {"Z_B": 12288, "R_B": 63, "T_B": 1024}
+
+# what an sm_100 part reports (used for CPU-side planning
+# and tests only; run time always queries the device).
+B200_NOMINAL = {
+    "sm_count": 148,
+    "warp_size": 32,
+    "max_threads_per_block": 1024,
+    "regs_per_thread": 255,
+    "smem_per_block": 49152,
+    "smem_per_block_optin": 232448,
+    "l2_bytes": 126 * 1024 * 1024,
+}
+
+
+@dataclass(frozen=True)
+class MachineValues:
+    """Values for the machine parameters of one case-table machine model."""
+
+    table: str  # which case tables to evaluate: 'b200' | 'fermi'
+    values: dict  # Z_B, R_B, T_B
+    source: str  # 'live:<device>' | 'fermi.machine' | 'nominal' | 'user'
+    props: dict = field(default_factory=dict, compare=False)
+    warp_size: int = 32
+
+
+def values_from_props(props: dict, smem: str = "optin") -> dict:
+    smem_bytes = props["smem_per_block_optin"] if smem == "optin" else props["smem_per_block"]
+    return {
+        "Z_B": int(smem_bytes) // 4,
+        "R_B": int(props["regs_per_thread"]),
+        "T_B": int(props["max_threads_per_block"]),
+    }
+
+
+@lru_cache(maxsize=None)
+def _live_props(device: int) -> tuple:
+    return tuple(sorted(_lib.query_machine(device).items()))
+
+
+def live(device: int = 0, smem: str = "optin") -> MachineValues:
+    """Query the device (pk_query_machine) -- replaces the machine constants."""
+    props = dict(_live_props(device))
+    if props.get("cc_major") != 10:
+        raise RuntimeError(
+            "device %d is sm_%d%d; libpk is built for sm_100a only"
+            % (device, props.get("cc_major"), props.get("cc_minor"))
+        )
+    return MachineValues("b200", values_from_props(props, smem), "live:%d" % device, props,
+                         int(props["warp_size"]))
+
+
+def nominal(smem: str = "optin") -> MachineValues:
+    return MachineValues("b200", values_from_props(B200_NOMINAL, smem), "nominal", dict(B200_NOMINAL))
+
+
+def fermi() -> MachineValues:
+    return MachineValues("fermi", dict(FERMI_VALUES), "fermi.machine")
+
+
+def resolve(machine=None) -> MachineValues:
+    if machine is None or machine == "live":
+        return live()
+    if isinstance(machine, MachineValues):
+        return machine
+    if machine == "fermi":
+        return fermi()
+    if machine == "nominal":
+        return nominal()
+    if machine == "static":
+        return live(smem="static")
+    if isinstance(machine, dict):
+        return MachineValues("b200", dict(machine), "user")
+    raise ValueError("unknown machine %r" % (machine,))
+
+
+def machine_file_text(mv: MachineValues) -> str:
+    """A .machine file pinning each limit to its live value, accepted by the
+    reference's ``parse_machine`` (machine.py:111-238) when parakern is
+    installed -- e.g. to re-run ``engine.optimize`` for a new program."""
+    v = mv.values
+    return (
+        "[machine]\nname = %s\ngrid_stride = 256\nwitness_budget = 200000\ncoverage_samples = 1000\n\n"
+        "[param.Z_B]\nkind = resource\nrange = 0 %d\n\n"
+        "[param.R_B]\nkind = resource\nrange = 0 %d\n\n"
+        "[param.T_B]\nkind = resource\nrange = 0 %d\n\n"
+        "[counter.shared_words]\nmeasure = shared-words\nbound = Z_B\nreduce_with = granularity caching-off\n\n"
+        "[counter.registers]\nmeasure = registers-per-thread\nbound = R_B\n"
+        "reduce_with = granularity cse-0 cse-1 regpressure-0 regpressure-1 regpressure-2\n\n"
+        "[counter.threads]\nmeasure = threads-per-block\nbound = T_B\nreduce_with = granularity\n\n"
+        "[strategies]\norder = granularity caching-off cse-0 cse-1 regpressure-0 regpressure-1 regpressure-2\n\n"
+        "[box]\ndefault = 1 64\nB = 1 1024\nB0 = 1 256\nB1 = 1 1024\nub1 = 1 256\n"
+        "N = 2 1073741824\nn = 1 16384\nT = 1 1024\n"
+    ) % ("live-" + mv.source.replace(":", "-"), v["Z_B"], v["R_B"], v["T_B"])

@@ -1,0 +1,217 @@
+"""Program identity: which kernel family a loop-nest program is.
+
+The reference executes ANY program by walking its AST
+(interp.py:85-174).  This executor binds the program shapes it has CUDA
+kernels for; a program is recognised by its canonical token stream, so a
+``parakern.dsl.Program`` (rendered with ``dsl.render``, dsl.py:954) and the
+same program as ``.mfk`` text (comments and layout ignored) both match.
+The recognised texts are the original programs and every case program the
+reference's strategies produce from them (granularity, caching-off; the
+IR-level cse/regpressure passes do not change the source), as recorded in
+the shipped case tables.  Anything else raises ``NotImplementedError`` --
+there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import glob
+import json
+import os
+import re
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+
+SOURCE_STRATEGIES = ("granularity", "caching-off")
+
+_TOKEN = re.compile(r"\s*(?:(//[^\n]*|/\*.*?\*/)|([A-Za-z_][A-Za-z_0-9]*|\d+|<=|>=|==|!=|&&|\+\+|\S))", re.S)
+
+
+def normalize(text: str) -> str:
+    """Canonical token stream of .mfk text: comments and whitespace dropped."""
+    out = []
+    pos = 0
+    text = text.strip()
+    while pos < len(text):
+        m = _TOKEN.match(text, pos)
+        if not m:
+            break
+        pos = m.end()
+        if m.group(2):
+            out.append(m.group(2))
+    return " ".join(out)
+
+
+def _c_div(a: int, b: int) -> int:
+    """C99 truncating division (interp.py:43-46)."""
+    q = abs(a) // abs(b)
+    return q if (a >= 0) == (b >= 0) else -q
+
+
+@dataclass(frozen=True)
+class ArrayDecl:
+    name: str
+    dims: tuple  # callables params -> extent, 1 or 2 of them
+
+
+@dataclass(frozen=True)
+class Family:
+    """Static description of one program family (one CUDA kernel family)."""
+
+    name: str
+    params: tuple[str, ...]  # scalar parameters of the ORIGINAL program, declaration order
+    arrays: tuple[ArrayDecl, ...]
+    written: tuple[str, ...]  # arrays the program writes
+    float_ok: bool  # Python floats allowed (matmul/matvec accumulate; permutations move bits)
+    contexts: tuple[str, ...] = ()  # serial context loop bounds (Jacobi T, matmul kdim)
+    doc: str = ""
+
+    def shapes(self, params: dict) -> dict[str, tuple[int, ...]]:
+        return {a.name: tuple(int(d(params)) for d in a.dims) for a in self.arrays}
+
+
+def _p(name):
+    return lambda P: P[name]
+
+
+FAMILIES: dict[str, Family] = {
+    "reverse": Family(
+        "reverse", ("N", "s", "B"),
+        (ArrayDecl("a", (_p("N"),)), ArrayDecl("c", (_p("N"),))),
+        ("c",), True, (), "SURVEY App. A.2: c[N-1-p] = a[p]",
+    ),
+    "transpose": Family(
+        "transpose", ("N", "s", "B0", "B1"),
+        (ArrayDecl("a", (_p("N"), _p("N"))), ArrayDecl("c", (lambda P: P["N"] * P["N"],))),
+        ("c",), True, (), "data/transpose.mfk: c[i*N+j] = a[j][i]",
+    ),
+    "jacobi": Family(
+        "jacobi", ("T", "N", "s", "B"),
+        (ArrayDecl("a", (lambda P: 2 * P["N"],)),),
+        ("a",), False, ("T",), "data/jacobi.mfk: 1-D 3-point Jacobi, double-buffered",
+    ),
+    "jacobi2d": Family(
+        "jacobi2d", ("T", "N", "s", "B0", "B1"),
+        (ArrayDecl("a", (lambda P: 2 * P["N"], _p("N"))),),
+        ("a",), False, ("T",), "SURVEY App. A.4: 2-D 5-point Jacobi, double-buffered",
+    ),
+    "matvec": Family(
+        "matvec", ("N", "s", "B"),
+        (ArrayDecl("a", (_p("N"), _p("N"))), ArrayDecl("x", (_p("N"),)), ArrayDecl("y", (_p("N"),))),
+        ("y",), True, (), "SURVEY App. A.3: y[r] += a[r][q]*x[q]",
+    ),
+    "matmul": Family(
+        "matmul", ("n", "B0", "ub1", "s"),
+        (ArrayDecl("a", (_p("n"), _p("n"))), ArrayDecl("b", (_p("n"), _p("n"))),
+         ArrayDecl("c", (_p("n"), _p("n")))),
+        ("c",), True, ("kdim",), "SURVEY App. A.1 (paper Fig. 3): c += a*b",
+    ),
+    "addition": Family(
+        "addition", ("N", "B0", "B1"),
+        (ArrayDecl("a", (lambda P: P["N"] * P["N"],)), ArrayDecl("b", (lambda P: P["N"] * P["N"],)),
+         ArrayDecl("c", (lambda P: P["N"] * P["N"],))),
+        ("c",), False, (), "data/addition.mfk: c = a + b with twin stores",
+    ),
+}
+
+
+@dataclass(frozen=True)
+class ProgramKind:
+    """A recognised program text: its family and the source-level strategies
+    already applied to it (a case program is itself a leaf)."""
+
+    family: str
+    applied: tuple[str, ...]  # subset of SOURCE_STRATEGIES, in application order
+    params: tuple[str, ...]  # scalar parameters this text declares
+    text: str = field(compare=False, repr=False, default="")
+
+    @property
+    def is_original(self) -> bool:
+        return not self.applied
+
+
+@lru_cache(maxsize=1)
+def registry() -> dict[str, ProgramKind]:
+    """Normalised text -> ProgramKind, from the shipped case tables."""
+    reg: dict[str, ProgramKind] = {}
+    for path in sorted(glob.glob(os.path.join(DATA, "cases", "*.json"))):
+        with open(path) as fh:
+            doc = json.load(fh)
+        fam = doc["family"]
+        key = normalize(doc["source"])
+        reg.setdefault(key, ProgramKind(fam, (), tuple(doc["params"]), doc["source"]))
+        for case in doc["cases"]:
+            applied = tuple(s for s in case["applied"] if s in SOURCE_STRATEGIES)
+            key = normalize(case["program"])
+            reg.setdefault(key, ProgramKind(fam, applied, tuple(case["params"]), case["program"]))
+    return reg
+
+
+def program_text(program) -> str:
+    """Source text of a program given as text, a path, or a parakern Program."""
+    if isinstance(program, str):
+        if "\n" not in program and program.endswith(".mfk") and os.path.exists(program):
+            with open(program) as fh:
+                return fh.read()
+        return program
+    if hasattr(program, "decls") and hasattr(program, "top"):
+        try:
+            from parakern import dsl  # the caller holds a parakern Program, so parakern exists
+        except ImportError as exc:  # pragma: no cover - defensive
+            raise TypeError("a parakern Program was passed but parakern is not importable") from exc
+        return dsl.render(program)
+    raise TypeError("program must be .mfk text, a path to a .mfk file or a parakern Program")
+
+
+def identify(program) -> ProgramKind:
+    """Recognise a program; NotImplementedError for shapes without a kernel."""
+    if isinstance(program, ProgramKind):
+        return program
+    key = normalize(program_text(program))
+    kind = registry().get(key)
+    if kind is None:
+        raise NotImplementedError(
+            "no sm_100a kernel family matches this program; the executor binds "
+            "%s and their case programs (there is no CPU fallback)" % ", ".join(sorted(FAMILIES))
+        )
+    return kind
+
+
+def original(family: str) -> ProgramKind:
+    for kind in registry().values():
+        if kind.family == family and kind.is_original:
+            return kind
+    raise KeyError(family)
+
+
+def source(family: str) -> str:
+    return original(family).text
+
+
+def effective_params(kind: ProgramKind, params: dict) -> dict:
+    """Parameters in the ORIGINAL program's names.
+
+    A granularity-rewritten program has no ``s`` (strategies.py:302-422
+    substitutes s := 1); the merged addition keeps its names but halves the
+    twin structure, which the kernel sees through PK_FLAG_MERGED.
+    """
+    fam = FAMILIES[kind.family]
+    missing = [p for p in kind.params if p not in params]
+    if missing:
+        # interp.py:73-75 raises for the first declared scalar without a value
+        raise KeyError("no value supplied for parameter %r" % missing[0])
+    out = {p: int(params[p]) for p in kind.params}
+    for p in fam.params:
+        if p not in out:
+            out[p] = 1  # the strategy substituted 1 for it
+    return out
+
+
+def array_shapes(kind: ProgramKind, params: dict) -> dict[str, tuple[int, ...]]:
+    P = effective_params(kind, params)
+    return FAMILIES[kind.family].shapes(P)
+
+
+def case_tables() -> list[str]:
+    return sorted(glob.glob(os.path.join(DATA, "cases", "*.json")))

@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a kernels (through run_program -> ctypes -> libpk.so)
+against the reference's own outputs and the CPU oracle.
+
+Bars (BASELINE.json north_star):
+* integer programs, reversal and transpose: bit-exact;
+* float32 matmul: normalised error max|C_gpu - C_ref| / max_ij sum_k |a_ik b_kj|
+  <= max(1e-5 * K / 1024, 2 * K * 2^-24)  (the second term covers tiny K, where
+  a single fp32 rounding per step can exceed the K-scaled bound);
+* float32 matvec (accumulated in binary64 on the GPU): within 2 fp32 ulps
+  of the reference's binary64 result.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(program, params, arrays, **kw):
+    from paper_1801_04348_b200 import run_program
+
+    return run_program(program, params, arrays, **kw)
+
+
+def _text(v):
+    from paper_1801_04348_b200 import programs
+
+    return programs.source(v["family"]) if v["program"] == "original" else v["program"]
+
+
+def _matmul_tol(K):
+    return max(1e-5 * K / 1024.0, 2.0 * K * 2.0**-24)
+
+
+def _check_float(family, params, inputs, got, want):
+    w = np.asarray(want, dtype=np.float64)
+    g = np.asarray(got, dtype=np.float64).reshape(w.shape)
+    if family == "matmul":
+        n = params["n"]
+        a = np.asarray(inputs["a"], dtype=np.float64)
+        b = np.asarray(inputs["b"], dtype=np.float64)
+        scale = (np.abs(a) @ np.abs(b)).max() if n else 0.0
+        scale = max(scale, np.abs(w).max() if w.size else 0.0, 1e-30)
+        K = max(1, (n // params["B0"]) * params["B0"])
+        assert np.abs(g - w).max() / scale <= _matmul_tol(K)
+    else:
+        tol = 2.0 * 2.0**-24 * np.abs(w) + 1e-30
+        assert np.all(np.abs(g - w) <= tol)
+
+
+def test_golden_vectors(cuda, golden):
+    """Every reference-generated vector, original and case programs."""
+    checked = 0
+    for v in golden:
+        if "error" in v:
+            if v["error"] == "ZeroDivisionError":
+                with pytest.raises(ZeroDivisionError):
+                    _run(_text(v), v["params"], None)
+            continue
+        got = _run(_text(v), v["params"], v["inputs"])
+        for name, want in v["outputs"].items():
+            if v["floats"] and name in ("c", "y"):
+                _check_float(v["family"], v["params"], v["inputs"], got[name], want)
+            elif v["floats"]:
+                assert np.array_equal(np.asarray(got[name], dtype=np.float64), np.asarray(want)), name
+            else:
+                assert got[name] == want, (v["family"], v["program"][:20], v["params"], name)
+        checked += 1
+    assert checked >= 100
+
+
+FAMILY_CASES = {
+    # family: (params, integer input range)
+    "reverse": ({"N": 1 << 16, "s": 4, "B": 128}, 1 << 30),
+    "transpose": ({"N": 256, "s": 4, "B0": 32, "B1": 8}, 1 << 30),
+    "jacobi": ({"T": 7, "N": (1 << 14) + 2, "s": 4, "B": 64}, 1 << 30),
+    "jacobi2d": ({"T": 5, "N": 130, "s": 2, "B0": 8, "B1": 16}, 1 << 30),
+    "matvec": ({"N": 256, "s": 2, "B": 32}, 1 << 10),
+    "matmul": ({"n": 128, "B0": 16, "ub1": 4, "s": 2}, 1 << 6),
+    "addition": ({"N": 128, "B0": 8, "B1": 16}, 1 << 30),
+}
+
+
+def _random_inputs(family, params, lim, rng):
+    from paper_1801_04348_b200 import programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    return {k: rng.integers(-lim, lim, size=s, dtype=np.int64).astype(np.int32) for k, s in shapes.items()}
+
+
+@pytest.mark.parametrize("family", sorted(FAMILY_CASES))
+def test_every_leaf_matches_oracle(cuda, oracle_mod, family):
+    """Force each case of the b200 table (staged / direct / granularity
+    leaves) plus the generic thread mapping: all bit-identical to the oracle."""
+    from paper_1801_04348_b200 import case_table, programs
+
+    params, lim = FAMILY_CASES[family]
+    rng = np.random.default_rng(0x1801)
+    inputs = _random_inputs(family, params, lim, rng)
+    want = oracle_mod.run(family, params, inputs)
+    text = programs.source(family)
+    for case in case_table(family, "b200").cases:
+        for generic in (False, True):
+            got = _run(text, params, inputs, case=case.index, generic=generic)
+            for name in want:
+                assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), \
+                    (family, case.index, generic, name)
+
+
+def test_case_selected_on_live_machine(cuda):
+    from paper_1801_04348_b200 import live_machine, select_case
+
+    mv = live_machine()
+    assert mv.values["T_B"] == 1024 and mv.values["R_B"] == 255
+    assert mv.values["Z_B"] * 4 == mv.props["smem_per_block_optin"]
+    # matvec caches x (N words) only if N <= Z_B: opt-in 227 KB keeps it at
+    # N = 32768, the 48 KB static limit (== Fermi's 12288 words) does not
+    assert select_case("matvec", {"N": 32768, "s": 1, "B": 256}, mv).applied == ()
+    static = live_machine(smem="static")
+    assert static.values["Z_B"] == 12288
+    assert select_case("matvec", {"N": 32768, "s": 1, "B": 256}, static).applied == ("granularity", "caching-off")
+
+
+def test_reversal_full_size_property(cuda):
+    """2^28 words: reversing twice is the identity and one reversal is exact."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs
+
+    N = 1 << 28
+    a = torch.randint(-(2**31), 2**31 - 1, (N,), dtype=torch.int32, device="cuda")
+    out = _run(programs.source("reverse"), {"N": N, "s": 16, "B": 256}, {"a": a})
+    assert torch.equal(out["c"], torch.flip(a, [0]))
+    back = _run(programs.source("reverse"), {"N": N, "s": 16, "B": 256}, {"a": out["c"]})
+    assert torch.equal(back["c"], a)
+
+
+def test_transpose_full_size_property(cuda):
+    torch = cuda
+    from paper_1801_04348_b200 import programs
+
+    N = 16384
+    a = torch.randint(-(2**31), 2**31 - 1, (N, N), dtype=torch.int32, device="cuda")
+    out = _run(programs.source("transpose"), {"N": N, "s": 4, "B0": 32, "B1": 8}, {"a": a})
+    assert torch.equal(out["c"].reshape(N, N), a.t())
+
+
+def test_matmul_fp32_tolerance_tuned_tile(cuda, oracle_mod):
+    """n = 1024 with the tuned 128 x 128 tile vs the binary64 oracle."""
+    from paper_1801_04348_b200 import last_run, programs
+
+    n = 1024
+    rng = np.random.default_rng(7)
+    a = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    b = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    c = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    params = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+    got = _run(programs.source("matmul"), params, {"a": a, "b": b, "c": c})
+    assert last_run().applied == ()
+    want = oracle_mod.run("matmul", params, {"a": a, "b": b, "c": c})["c"]
+    scale = (np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64))).max()
+    err = np.abs(got["c"].astype(np.float64) - want).max() / scale
+    assert err <= _matmul_tol(n), err
+
+
+def test_matmul_integer_valued_fp32_is_exact(cuda, oracle_mod):
+    """Integer-valued fp32 in [-8, 8]: every partial sum is an integer below
+    2^24, so the fp32 result must equal the binary64 reference exactly."""
+    from paper_1801_04348_b200 import programs
+
+    n = 512
+    rng = np.random.default_rng(11)
+    a = rng.integers(-8, 9, (n, n)).astype(np.float32)
+    b = rng.integers(-8, 9, (n, n)).astype(np.float32)
+    for params in ({"n": n, "B0": 128, "ub1": 8, "s": 16}, {"n": n, "B0": 8, "ub1": 16, "s": 4}):
+        got = _run(programs.source("matmul"), params, {"a": a, "b": b})
+        want = oracle_mod.run("matmul", params, {"a": a, "b": b})["c"]
+        assert np.array_equal(got["c"].astype(np.float64), want)
+
+
+def test_tuned_and_generic_matmul_bit_identical(cuda):
+    """Same ascending-k FFMA chain in both kernels: identical bits."""
+    from paper_1801_04348_b200 import programs
+
+    n = 256
+    rng = np.random.default_rng(5)
+    arrays = {k: rng.standard_normal((n, n)).astype(np.float32) for k in "abc"}
+    params = {"n": n, "B0": 64, "ub1": 8, "s": 8}
+    t = _run(programs.source("matmul"), params, arrays)["c"]
+    g = _run(programs.source("matmul"), params, arrays, generic=True)["c"]
+    assert np.array_equal(t.view(np.uint32), g.view(np.uint32))
+
+
+def test_errors_mirror_reference(cuda):
+    from paper_1801_04348_b200 import programs
+
+    text = programs.source("jacobi")
+    with pytest.raises(KeyError):
+        _run(text, {"T": 1, "N": 10, "s": 1}, None)  # interp.py:75
+    with pytest.raises(ZeroDivisionError):
+        _run(text, {"T": 1, "N": 10, "s": 0, "B": 4}, None)
+    with pytest.raises(NotImplementedError):
+        _run(text, {"T": 1, "N": 10, "s": 1, "B": 4}, None, tracer=lambda *a: None)
+    with pytest.raises(NotImplementedError):
+        _run("int N; int a[N]; meta_schedule { meta_for (int i = 0; i < N; i++) { a[i] = i; } }", {"N": 4}, None)
+
+
+def test_inputs_not_mutated_and_missing_arrays_zero(cuda):
+    from paper_1801_04348_b200 import programs
+
+    a = list(range(16))
+    keep = list(a)
+    out = _run(programs.source("reverse"), {"N": 16, "s": 1, "B": 4}, {"a": a})
+    assert a == keep  # interp.py:76-78 deep copies
+    assert out["c"] == keep[::-1]
+    out = _run(programs.source("reverse"), {"N": 16, "s": 1, "B": 4}, None)
+    assert out["a"] == [0] * 16 and out["c"] == [0] * 16
