@@ -1,0 +1,383 @@
+"""bench.py -- the driver's benchmark contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload matmul8192|matmul2048|matmul1024|jacobi|jacobi2d|reverse|transpose|matvec]
+
+Headline workload (BASELINE.json configs[1]): FP32 matrix multiplication
+n = 8192, program parameters auto-tuned inside the case the live B200
+selects, rows of c sharded over the ranks (strong scaling: n is fixed).
+A "step" is one pass of the hot path: one pk_launch of the selected leaf
+over the resident inputs (c += a*b).  ``value`` is whole-job GFLOP/s from
+CUDA events (max over ranks); ``e2e`` is the same metric through the C-ABI
+host-buffer entry point pk_run_host with pinned host buffers (H2D of every
+input and D2H of c inside the timed region).  The other BASELINE configs
+(reversal, transpose, 1-D/2-D Jacobi, mat-vec) are measured in the same run
+under ``kernels`` on rank 0 at N=1.
+
+``--impl reference`` times the reference path's CPU restatement (the
+oracle port, oracle/pk_oracle.c, all host threads) on a bounded sample of
+the same workload -- the reference itself is a pure-Python interpreter
+with no compiled form.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+METRIC = "matmul GFLOP/s & stencil/reversal HBM GB/s, case-selected kernels, 1/2/4/8 B200"
+
+# BASELINE.json configs measured under "kernels" (family, params, algorithmic bytes or flops)
+KERNEL_CONFIGS = {
+    "reverse": ({"N": 1 << 30, "s": 16, "B": 256}, 8 * (1 << 30), "GB/s"),
+    "transpose": ({"N": 32768, "s": 8, "B0": 64, "B1": 8}, 8 * 32768 * 32768, "GB/s"),
+    "jacobi": ({"T": 100, "N": (1 << 28) + 2, "s": 16, "B": 256}, 100 * 8 * (1 << 28), "GB/s"),
+    "jacobi2d": ({"T": 50, "N": 16386, "s": 4, "B0": 8, "B1": 32}, 50 * 8 * 16384 * 16384, "GB/s"),
+    "matvec": ({"N": 32768, "s": 1, "B": 128}, 4 * 32768 * 32768 + 8 * 32768, "GB/s"),
+}
+
+
+def load_peaks() -> dict:
+    try:
+        with open(MEASURED_PEAKS) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers ----
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def timed_cpu(fn, budget_s: float, min_runs: int = 1):
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        fn()
+        runs += 1
+        el = time.perf_counter() - t0
+        if runs >= min_runs and el >= budget_s:
+            return el / runs, runs
+        if el > budget_s * 3:
+            return el / runs, runs
+
+
+def cpu_matmul_sample(n: int, threads: int, budget_s: float):
+    """Oracle port (binary64, interpreter order) on an n x n sample."""
+    import numpy as np
+
+    from oracle import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    rng = np.random.default_rng(0x1801)
+    a = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    b = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    P = {"n": n, "B0": 128 if n >= 128 else n, "ub1": 8 if n >= 128 else 1, "s": 16 if n >= 128 else 1}
+    sec, runs = timed_cpu(lambda: oracle.run("matmul", P, {"a": a, "b": b}), budget_s)
+    return 2.0 * n**3 / sec / 1e9, runs, sec
+
+
+# ------------------------------------------------------------- reference ----
+
+def run_reference(args) -> int:
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return 0
+    n_sample = 1024
+    threads = cpu_cores()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gflops, runs, sec = cpu_matmul_sample(n_sample, threads, budget_s=0.0)
+        if i >= args.warmup:
+            vals.append((gflops, sec))
+    gf = statistics.median(v[0] for v in vals)
+    ms = statistics.median(v[1] for v in vals) * 1e3
+    sample = "matmul n=%d per step (2n^3 = %.3g FLOP), binary64 ascending-k, of the n=%d workload" % (
+        n_sample, 2.0 * n_sample**3, args.n)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": round(gf, 3), "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic U[-1,1) fp32 inputs, seed 0x1801",
+        "config": {"workload": "matmul n=%d fp32 (CPU sample n=%d)" % (args.n, n_sample),
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(gf, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- ours ----
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-family extras")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1801_04348_b200 import _lib, autotune, binding, cases, programs
+    from paper_1801_04348_b200 import machine as machine_mod
+
+    rank, world, local = dist_info()
+    if world != args.gpus and world > 1:
+        print("warning: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus), file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    mv = machine_mod.live(local)
+
+    n = args.n
+    kind = programs.original("matmul")
+    base = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+    g = torch.Generator(device=dev)
+    g.manual_seed(0x1801 + rank)
+    # row shard of a and c, full b (resident; no data-path collective)
+    rows = n // world
+    r0 = rank * rows
+    a = torch.rand(n * n, device=dev, generator=g) * 2 - 1  # full-size buffers, rank owns its rows
+    b = torch.rand(n * n, device=dev, generator=g) * 2 - 1
+    c = torch.zeros(n * n, device=dev)
+    ptrs = [a.data_ptr(), b.data_ptr(), c.data_ptr()]
+
+    # tune (B0, ub1, s) inside the selected case, on this rank's shard
+    grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in
+            ((128, 8, 16), (128, 8, 8), (64, 8, 16), (64, 8, 8), (64, 16, 8))]
+    tuned, trials = autotune.autotune(kind, base, machine=mv, buffers=[a, b, c], reps=2, grid=grid)
+    sel = cases.select(kind, tuned, mv)
+    L = binding.make_launch(kind, tuned, sel.applied, _lib.DTYPE_F32, lo=r0, hi=r0 + rows)
+    stream = torch.cuda.current_stream(dev)
+    st = stream.cuda_stream
+
+    for _ in range(max(3, args.warmup)):
+        _lib.launch(L, ptrs, st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            _lib.launch(L, ptrs, st)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms_local = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_total = float(ms_t.item())
+    ms_step = ms_total / args.steps
+    flop_step = 2.0 * n * n * n  # whole job, all ranks
+    value = flop_step / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant (only) kernel: FP32 FFMA pipe
+    per_launch_flop = 2.0 * rows * n * n
+    achieved_tf = per_launch_flop / (ms_local / args.steps * 1e-3) / 1e12
+    sm_count = mv.props.get("sm_count", 148)
+    peak_tf = sm_count * 256 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    clocks = clk.summary()
+    peak_at_clock = sm_count * 256 * clocks["sm_mhz"] * 1e6 / 1e12 if clocks["sm_mhz"] else None
+
+    # e2e through the C-ABI host-buffer call (pinned host memory)
+    e2e = None
+    ha = torch.empty(n * n, dtype=torch.float32, pin_memory=True)
+    hb = torch.empty(n * n, dtype=torch.float32, pin_memory=True)
+    hc = torch.zeros(n * n, dtype=torch.float32, pin_memory=True)
+    ha.copy_(a.cpu())
+    hb.copy_(b.cpu())
+    Lh = binding.make_launch(kind, tuned, sel.applied, _lib.DTYPE_F32, lo=r0, hi=r0 + rows)
+    hp = [ha.data_ptr(), hb.data_ptr(), hc.data_ptr()]
+    _lib.run_host(Lh, hp, local)  # warm the allocator pool
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        _lib.run_host(Lh, hp, local)
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_gf = flop_step / float(e2e_s.item()) / 1e9
+    e2e = {"value": round(e2e_gf, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": 3 * n * n * 4 * world,
+           "d2h_bytes_per_step": n * n * 4 * world,
+           "path": "pk_run_host (C ABI) with pinned host buffers; pk_run_host copies the full arrays"}
+
+    kernels = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_kernels:
+        del ha, hb, hc
+        kernels = bench_kernels(peaks, mv)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = cpu_cores()
+        gf, runs, sec = cpu_matmul_sample(1024, threads, budget_s=10.0)
+        cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+               "sample": "oracle/pk_oracle.c binary64 matmul n=1024 (2.15 GFLOP) x %d runs, %.1f s/run; "
+                         "the reference interpreter itself ran 46k FMA/s on 1 core (SURVEY 6)" % (runs, sec)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic U[-1,1) fp32, seed 0x1801+rank",
+            "config": {"workload": "matmul n=%d fp32 FFMA, (B0,ub1,s) auto-tuned inside the live case" % n,
+                       "n": n, "tuned": tuned, "case": sel.index, "applied": list(sel.applied),
+                       "machine": mv.values, "parallelism": "row-shard x%d" % world,
+                       "l2": "inputs (3 x %d MiB) larger than L2" % (n * n * 4 >> 20),
+                       "trials": [[t.params["B0"], t.params["ub1"], t.params["s"], round(t.ms, 3)] for t in trials]},
+            "roofline": {"bound": "fp32-fma", "achieved": round(achieved_tf, 2),
+                         "peak": round(peak_tf, 2), "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
+                         "peak_source": "computed: %d SM x 256 FLOP/clk x %.0f MHz max clock "
+                                        "(MEASURED_PEAKS.json has no FP32 figure)" % (sm_count, peaks["sm_max_mhz"]),
+                         "frac_at_observed_clock": round(achieved_tf / peak_at_clock, 4) if peak_at_clock else None,
+                         "traffic": None},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "kernels": kernels,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_kernels(peaks, mv) -> dict:
+    """The bandwidth-bound BASELINE configs on one GPU: GB/s of algorithmic
+    traffic and the fraction of the measured copy bandwidth."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, binding, cases, programs
+
+    out = {}
+    for fam, (params, work, unit) in KERNEL_CONFIGS.items():
+        kind = programs.original(fam)
+        sel = cases.select(kind, params, mv)
+        L = binding.make_launch(kind, params, sel.applied, _lib.DTYPE_I32)
+        shapes = programs.array_shapes(kind, params)
+        bufs = []
+        for arr in programs.FAMILIES[fam].arrays:
+            n = 1
+            for d in shapes[arr.name]:
+                n *= d
+            bufs.append(torch.randint(-(1 << 20), 1 << 20, (n,), dtype=torch.int32, device="cuda"))
+        ptrs = [x.data_ptr() for x in bufs]
+        st = torch.cuda.current_stream()
+        _lib.launch(L, ptrs, st.cuda_stream)
+        torch.cuda.synchronize()
+        reps = 1 if fam.startswith("jacobi") else 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            _lib.launch(L, ptrs, st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = work / (ms * 1e-3) / 1e9
+        out[fam] = {"params": params, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
+                    "value": round(gbs, 1), "unit": unit, "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
+                    "frac_of_8tbs": round(gbs / 8000.0, 4)}
+        del bufs
+        torch.cuda.empty_cache()
+    return out
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

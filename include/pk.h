@@ -53,6 +53,10 @@ extern "C" {
 #define PK_FLAG_MERGED 0x4      /* addition only: twin stores merged by granularity          */
 #define PK_FLAG_GENERIC 0x8     /* force the generic (one thread per paper thread) kernel    */
 #define PK_FLAG_TF32X3 0x10     /* matmul f32 only: 3xTF32 on tcgen05 (reported apart)       */
+#define PK_FLAG_NARROW 0x20     /* Jacobi only: caller guarantees |v| <= (2^31-1)/3 (1-D) or
+                                   /5 (2-D) for every value, so int32 sums are exact
+                                   (pk_jacobi_narrow checks it); without it pk_launch checks
+                                   on the device and pk_jacobi_sweep forms 64-bit sums     */
 
 /* ---- element types ------------------------------------------------------- */
 #define PK_DTYPE_I32 0 /* the DSL's int: C int32 arithmetic, truncating / and % */
@@ -131,6 +135,12 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
  * 2-D are the program's covered columns.  Uses the tile geometry of L. */
 int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
                     void *stream);
+
+/* Value-range check for the Jacobi fast path: *narrow = 1 when every value
+ * of the double buffer `a` is within the PK_FLAG_NARROW bound (a Jacobi
+ * average never leaves the range of its inputs, so the bound then holds for
+ * every later step too).  Synchronises `stream`. */
+int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void *stream);
 
 /* Shared-memory words the leaf kernel stages per block (the footprint the
  * case constrains against Z_B; reference counters.py:416-464). */

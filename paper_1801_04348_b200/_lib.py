@@ -42,6 +42,7 @@ FLAG_TEMPORAL = 0x2
 FLAG_MERGED = 0x4
 FLAG_GENERIC = 0x8
 FLAG_TF32X3 = 0x10
+FLAG_NARROW = 0x20
 
 DTYPE_I32 = 0
 DTYPE_F32 = 1
@@ -52,6 +53,7 @@ EXPORTS = (
     "pk_launch",
     "pk_run_host",
     "pk_jacobi_sweep",
+    "pk_jacobi_narrow",
     "pk_footprint_words",
     "pk_launch_count",
     "pk_last_error",
@@ -136,6 +138,8 @@ def load() -> ctypes.CDLL:
         lib.pk_run_host.restype = ctypes.c_int
         lib.pk_jacobi_sweep.argtypes = [ctypes.POINTER(PkLaunch), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
         lib.pk_jacobi_sweep.restype = ctypes.c_int
+        lib.pk_jacobi_narrow.argtypes = [ctypes.POINTER(PkLaunch), vp, ctypes.POINTER(ctypes.c_int32), vp]
+        lib.pk_jacobi_narrow.restype = ctypes.c_int
         lib.pk_footprint_words.argtypes = [ctypes.POINTER(PkLaunch)]
         lib.pk_footprint_words.restype = ctypes.c_int64
         lib.pk_launch_count.argtypes = []
@@ -194,6 +198,13 @@ def jacobi_sweep(L: PkLaunch, src: int, dst: int, lo: int, hi: int, stream: int 
     lib = load()
     check(lib.pk_jacobi_sweep(ctypes.byref(L), ctypes.c_void_p(src), ctypes.c_void_p(dst), lo, hi,
                               ctypes.c_void_p(stream or None)))
+
+
+def jacobi_narrow(L: PkLaunch, a: int, stream: int = 0) -> bool:
+    out = ctypes.c_int32(0)
+    check(load().pk_jacobi_narrow(ctypes.byref(L), ctypes.c_void_p(a), ctypes.byref(out),
+                                  ctypes.c_void_p(stream or None)))
+    return bool(out.value)
 
 
 def footprint_words(L: PkLaunch) -> int:

@@ -1,0 +1,131 @@
+"""Auto-tuner: sweep program parameters INSIDE the selected case.
+
+The paper's case discussion leaves the program parameters (block format
+B / B0 x B1 / B0 x ub1, granularity s) free within each case.  The tuner
+times candidate assignments on the device and keeps the fastest, subject to:
+
+1. equal coverage -- the candidate writes exactly the elements the caller's
+   parameters write (``programs.coverage``), so results are unchanged;
+2. a case of the discussion holds at the live machine values (no fallback),
+   and, with ``same_case=True``, it is the case the caller's point selects;
+3. the executor-side warp rule the reference cannot express (no warp-size
+   machine parameter, counters.py:66): threads per block a multiple of the
+   live warp size.
+
+Timing uses CUDA events around pk_launch on the current stream.
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass
+
+from . import _lib, binding, cases, programs
+from . import machine as machine_mod
+
+GRID = {
+    "reverse": {"B": [128, 256, 512, 1024], "s": [4, 8, 16, 32, 64]},
+    "jacobi": {"B": [128, 256, 512, 1024], "s": [2, 4, 8, 16, 32]},
+    "matvec": {"B": [128, 256, 512, 1024], "s": [1, 2, 4, 8]},
+    "transpose": {"B0": [16, 32, 64, 128], "B1": [8, 16, 32], "s": [1, 2, 4, 8]},
+    "jacobi2d": {"B0": [1, 2, 4, 8, 16], "B1": [32, 64, 128, 256], "s": [1, 2, 4, 8]},
+    "matmul": {"B0": [64, 128], "ub1": [4, 8, 16], "s": [4, 8, 16, 32]},
+    "addition": {"B0": [1, 2, 4, 8], "B1": [32, 64, 128, 256]},
+}
+
+
+@dataclass
+class Trial:
+    params: dict
+    case: int
+    applied: tuple
+    ms: float
+
+
+def candidates(family: str, base: dict, mv, *, same_case: bool = False, grid=None):
+    """Parameter assignments that keep coverage and select a real case."""
+    grid = grid or GRID[family]
+    want = programs.coverage(family, base)
+    base_case = cases.select(family, base, mv).index if same_case else None
+    if isinstance(grid, dict):
+        keys = sorted(grid)
+        points = [dict(zip(keys, combo)) for combo in itertools.product(*(grid[k] for k in keys))]
+    else:  # an explicit list of assignments
+        points = [dict(p) for p in grid]
+    out = []
+    for pt in points:
+        P = dict(base)
+        P.update(pt)
+        try:
+            if programs.coverage(family, P) != want:
+                continue
+        except ZeroDivisionError:
+            continue
+        if programs.threads_per_block(family, P) % mv.warp_size:
+            continue
+        sel = cases.select(family, P, mv)
+        if sel.fallback or (base_case is not None and sel.index != base_case):
+            continue
+        out.append((P, sel))
+    return out
+
+
+def time_launch(L, ptrs, reps: int = 3, warmup: int = 1) -> float:
+    import torch
+
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def autotune(program, params: dict, *, machine=None, dtype=None, buffers=None, reps: int = 3,
+             same_case: bool = False, grid=None, max_trials: int | None = None):
+    """Return (best_params, trials) for ``program`` at ``params``.
+
+    ``buffers``: device tensors in declaration order (allocated with random
+    data when omitted).  The caller's data is never needed: tuning runs on
+    scratch buffers of the same shapes.
+    """
+    import torch
+
+    kind = programs.identify(program) if not isinstance(program, str) or "\n" in program or program not in programs.FAMILIES \
+        else programs.original(program)
+    P0 = programs.effective_params(kind, params)
+    mv = machine_mod.resolve(machine)
+    fam = programs.FAMILIES[kind.family]
+    if dtype is None:
+        dtype = _lib.DTYPE_F32 if kind.family == "matmul" else _lib.DTYPE_I32
+    if buffers is None:
+        shapes = fam.shapes(P0)
+        buffers = []
+        for a in fam.arrays:
+            n = 1
+            for d in shapes[a.name]:
+                n *= d
+            if dtype == _lib.DTYPE_F32:
+                buffers.append(torch.rand(n, device="cuda") - 0.5)
+            else:
+                buffers.append(torch.randint(-1000, 1000, (n,), dtype=torch.int32, device="cuda"))
+    ptrs = [b.data_ptr() for b in buffers]
+    trials = []
+    cands = candidates(kind.family, P0, mv, same_case=same_case, grid=grid)
+    if max_trials:
+        cands = cands[:max_trials]
+    for P, sel in cands:
+        L = binding.make_launch(kind, P, sel.applied, dtype)
+        try:
+            ms = time_launch(L, ptrs, reps)
+        except (ValueError, NotImplementedError):
+            continue
+        trials.append(Trial(P, sel.index, sel.applied, ms))
+    if not trials:
+        return P0, trials
+    best = min(trials, key=lambda t: t.ms)
+    return best.params, trials

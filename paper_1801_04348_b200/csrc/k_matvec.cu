@@ -1,14 +1,17 @@
 // k_matvec.cu -- matrix-vector product (SURVEY App. A.3 matvec.mfk):
 //   dim = N/(s*B);  r = i*s*B + k*B + j < dim*s*B;  for q < N: y[r] = y[r] + a[r][q]*x[q]
-// A block owns E*B consecutive rows (E = s, or 1 after granularity).  Each
-// row is reduced by a group of lanes (a full warp when B allows) reading the
-// row with 128-bit loads, then combined with warp shuffles.  cache(x) kept:
-// x is staged once per block in shared memory (N words; the case requires
-// N <= Z_B); caching-off reads x through L1/L2.
-// Integers accumulate in wrapping int32 -- exact whenever the result fits,
-// as two's-complement sums are exact modulo 2^32.  float32 data accumulate
-// in binary64 (the reference sums Python floats), rounded once at the end.
-// HBM-bound: 4*N bytes of a per row dominate (x stays in L2/shared memory).
+// A block owns E*B consecutive rows (E = s, or 1 after granularity).  Rows are
+// reduced by groups of lanes (a full warp when B allows): each group walks R
+// rows at once with U 128-bit loads per row in flight, so a warp keeps R*U*512
+// bytes of a outstanding -- the memory-level parallelism a tall mat-vec needs
+// when the staged x (N words of shared memory) leaves room for only one block
+// per SM.  Partial sums meet in warp shuffles.
+// cache(x) kept: x is staged once per block in shared memory (the case
+// requires N <= Z_B); caching-off reads x through L1/L2.
+// Integers accumulate in wrapping int32 -- exact whenever the result fits, as
+// two's-complement sums are exact modulo 2^32.  float32 data accumulate in
+// binary64 (the reference sums Python floats), rounded once at the end.
+// HBM-bound: 4*N bytes of a per row dominate (x stays on chip).
 #include "pk_internal.cuh"
 
 namespace pk {
@@ -24,8 +27,21 @@ __device__ __forceinline__ A group_sum(A v, int lanes) {
     return v;
 }
 
+template <typename A, typename T>
+__device__ __forceinline__ A dot4(const int4 &av, const T *xp) {
+    const T *ap = reinterpret_cast<const T *>(&av);
+    A s = (A)ap[0] * (A)xp[0];
+    s += (A)ap[1] * (A)xp[1];
+    s += (A)ap[2] * (A)xp[2];
+    s += (A)ap[3] * (A)xp[3];
+    return s;
+}
+
+constexpr int kRows = 4;    // rows per lane group in flight
+constexpr int kUnroll = 4;  // 128-bit loads per row in flight
+
 template <typename T, bool STAGED, bool VEC>
-__global__ void __launch_bounds__(1024) k_matvec(const T *__restrict__ a, const T *__restrict__ x,
+__global__ void __launch_bounds__(256) k_matvec(const T *__restrict__ a, const T *__restrict__ x,
                                                 T *__restrict__ y, int64_t N, int64_t rlo,
                                                 int64_t rhi, int tile, int lanes) {
     using A = typename Acc<T>::type;
@@ -47,27 +63,52 @@ __global__ void __launch_bounds__(1024) k_matvec(const T *__restrict__ a, const 
     const int64_t end = min(base + tile, rhi);
     const int lane = threadIdx.x % lanes, group = threadIdx.x / lanes;
     const int ngroups = blockDim.x / lanes;
-    for (int64_t r = base + group; r < end; r += ngroups) {
-        const T *row = a + r * N;
-        A acc = 0;
+    for (int64_t r0 = base + (int64_t)group * kRows; r0 < end; r0 += (int64_t)ngroups * kRows) {
+        const int nr = (int)min((int64_t)kRows, end - r0);
+        A acc[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; i++) acc[i] = 0;
         if (VEC) {
             const int64_t n4 = N / 4;
-#pragma unroll 4
-            for (int64_t q = lane; q < n4; q += lanes) {
-                const int4 av = ld_stream(reinterpret_cast<const int4 *>(row) + q);
-                const T *ap = reinterpret_cast<const T *>(&av);
-                const T *xp = xs + 4 * q;
-                acc += (A)ap[0] * (A)xp[0];
-                acc += (A)ap[1] * (A)xp[1];
-                acc += (A)ap[2] * (A)xp[2];
-                acc += (A)ap[3] * (A)xp[3];
+            const int4 *rows[kRows];
+#pragma unroll
+            for (int i = 0; i < kRows; i++)
+                rows[i] = reinterpret_cast<const int4 *>(a + (r0 + (i < nr ? i : 0)) * N);
+            const int4 *xv = reinterpret_cast<const int4 *>(xs);
+            for (int64_t q0 = lane; q0 < n4; q0 += (int64_t)lanes * kUnroll) {
+                int4 v[kUnroll][kRows];
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int64_t q = q0 + (int64_t)u * lanes;
+#pragma unroll
+                    for (int i = 0; i < kRows; i++)
+                        v[u][i] = (q < n4 && i < nr) ? ld_stream(rows[i] + q) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    const int64_t q = q0 + (int64_t)u * lanes;
+                    if (q < n4) {
+                        const int4 xq = xv[q];
+                        const T *xp = reinterpret_cast<const T *>(&xq);
+#pragma unroll
+                        for (int i = 0; i < kRows; i++) acc[i] += dot4<A, T>(v[u][i], xp);
+                    }
+                }
             }
         } else {
-#pragma unroll 4
-            for (int64_t q = lane; q < N; q += lanes) acc += (A)row[q] * (A)xs[q];
+#pragma unroll
+            for (int i = 0; i < kRows; i++) {
+                if (i < nr) {
+                    const T *row = a + (r0 + i) * N;
+                    for (int64_t q = lane; q < N; q += lanes) acc[i] += (A)row[q] * (A)xs[q];
+                }
+            }
         }
-        acc = group_sum(acc, lanes);
-        if (lane == 0) y[r] = (T)((A)y[r] + acc);
+#pragma unroll
+        for (int i = 0; i < kRows; i++) {
+            const A sum = group_sum(acc[i], lanes);
+            if (lane == 0 && i < nr) y[r0 + i] = (T)((A)y[r0 + i] + sum);
+        }
     }
 }
 
@@ -76,7 +117,7 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     const int64_t tile64 = elems(L) * L.B;
     if (tile64 > (1 << 30)) return fail(PK_E_UNSUPPORTED, "matvec: tile too large");
     const int tile = (int)tile64;
-    int nt = (int)(L.B < 1024 ? L.B : 1024);
+    int nt = (int)(L.B < 256 ? L.B : 256);  // groups loop over the tile, so 256 threads cover any B
     // lanes per row: the largest power of two <= 32 dividing the block size
     int lanes = 1;
     while (lanes < 32 && nt % (lanes * 2) == 0) lanes *= 2;

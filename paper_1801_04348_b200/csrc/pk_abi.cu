@@ -172,6 +172,13 @@ int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo
     return fail(PK_E_PARAM, "pk_jacobi_sweep: family %d is not a Jacobi stencil", L->family);
 }
 
+int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void *stream) {
+    if (!L || !a || !narrow) return fail(PK_E_PARAM, "null argument");
+    if (L->family != PK_FAMILY_JACOBI1D && L->family != PK_FAMILY_JACOBI2D)
+        return fail(PK_E_PARAM, "pk_jacobi_narrow: family %d is not a Jacobi stencil", L->family);
+    return jacobi_narrow(*L, a, narrow, static_cast<cudaStream_t>(stream));
+}
+
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device) {
     int rc = validate(L, nptrs);
     if (rc) return rc;

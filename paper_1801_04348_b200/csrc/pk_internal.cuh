@@ -59,6 +59,7 @@ int sweep_jacobi1d(const pk_launch_t &L, const void *src, void *dst, int64_t lo,
                    cudaStream_t st);
 int sweep_jacobi2d(const pk_launch_t &L, const void *src, void *dst, int64_t lo, int64_t hi,
                    cudaStream_t st);
+int jacobi_narrow(const pk_launch_t &L, const void *a, int *narrow, cudaStream_t st);
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);

@@ -215,3 +215,38 @@ def array_shapes(kind: ProgramKind, params: dict) -> dict[str, tuple[int, ...]]:
 
 def case_tables() -> list[str]:
     return sorted(glob.glob(os.path.join(DATA, "cases", "*.json")))
+
+
+def coverage(family: str, P: dict) -> tuple:
+    """The index sets a run writes (and, for matmul, the reduction length),
+    from the program's bindings with C division.  Two parameter choices with
+    equal coverage compute identical results, so the tuner may swap them."""
+    def cover(extent, tile):
+        if tile <= 0:
+            return None
+        return max(0, _c_div(extent, tile)) * tile
+
+    if family == "reverse":
+        return (P["N"], cover(P["N"], P["s"] * P["B"]))
+    if family == "transpose":
+        return (P["N"], cover(P["N"], P["B0"]), cover(P["N"], P["s"] * P["B1"]))
+    if family == "jacobi":
+        return (P["N"], P["T"], cover(P["N"] - 2, P["s"] * P["B"]))
+    if family == "jacobi2d":
+        return (P["N"], P["T"], cover(P["N"] - 2, P["B0"]), cover(P["N"] - 2, P["s"] * P["B1"]))
+    if family == "matvec":
+        return (P["N"], cover(P["N"], P["s"] * P["B"]))
+    if family == "matmul":
+        return (P["n"], cover(P["n"], P["B0"]), cover(P["n"], P["ub1"] * P["s"]))
+    if family == "addition":
+        return (P["N"], cover(P["N"], P["B0"]), cover(P["N"], 2 * P["B1"]))
+    raise KeyError(family)
+
+
+def threads_per_block(family: str, P: dict) -> int:
+    """The program's thread-block size (product of the thread meta_for bounds)."""
+    if family in ("reverse", "jacobi", "matvec"):
+        return P["B"]
+    if family == "matmul":
+        return P["B0"] * P["ub1"]
+    return P["B0"] * P["B1"]

@@ -1,0 +1,105 @@
+"""Partitioned execution on one GPU: every rank's unit range launched through
+pk_launch(lo, hi) / pk_jacobi_sweep, ranks simulated in-process (the box has
+one GPU; the same schedule runs one process per GPU over NCCL in bench.py)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, arr):
+    return torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).cuda()
+
+
+@pytest.mark.parametrize("family,params", [
+    ("reverse", {"N": 1 << 16, "s": 4, "B": 64}),
+    ("transpose", {"N": 512, "s": 4, "B0": 32, "B1": 8}),
+    ("matvec", {"N": 512, "s": 2, "B": 64}),
+    ("matmul", {"n": 512, "B0": 64, "ub1": 8, "s": 16}),
+    ("addition", {"N": 256, "B0": 4, "B1": 64}),
+])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_shards_reassemble_full_run(cuda, family, params, world):
+    torch = cuda
+    from paper_1801_04348_b200 import _lib, binding, cases, partition, programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    rng = np.random.default_rng(world)
+    init = {k: rng.integers(-64, 64, size=s).astype(np.int32) for k, s in shapes.items()}
+    sel = cases.select(kind, params, "nominal")
+    full = [_dev(torch, init[a.name]) for a in programs.FAMILIES[family].arrays]
+    _lib.launch(binding.make_launch(kind, params, sel.applied), [t.data_ptr() for t in full])
+    shard = [_dev(torch, init[a.name]) for a in programs.FAMILIES[family].arrays]
+    for r in range(world):
+        lo, hi = partition.split(family, params, r, world)
+        if hi > lo:
+            L = binding.make_launch(kind, params, sel.applied, lo=lo, hi=hi)
+            _lib.launch(L, [t.data_ptr() for t in shard])
+    torch.cuda.synchronize()
+    for f, s in zip(full, shard):
+        assert torch.equal(f, s)
+
+
+@pytest.mark.parametrize("family,params", [
+    ("jacobi", {"T": 11, "N": (1 << 16) + 2, "s": 4, "B": 64}),
+    ("jacobi", {"T": 5, "N": 1001, "s": 2, "B": 16}),  # tail and odd N (scalar path)
+    ("jacobi2d", {"T": 7, "N": 258, "s": 2, "B0": 8, "B1": 16}),
+    ("jacobi2d", {"T": 4, "N": 67, "s": 1, "B0": 4, "B1": 8}),
+])
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_halo_exchange_ranks_match_oracle(cuda, oracle_mod, family, params, world):
+    torch = cuda
+    from paper_1801_04348_b200 import _lib, binding, cases, partition, programs
+
+    kind = programs.original(family)
+    N = params["N"]
+    size = 2 * N if family == "jacobi" else 2 * N * N
+    rng = np.random.default_rng(17)
+    init = rng.integers(-(1 << 20), 1 << 20, size=size).astype(np.int32)
+    want = np.asarray(oracle_mod.run(family, params, {"a": init.reshape((-1,) if family == "jacobi" else (2 * N, N))})["a"]).reshape(-1)
+    sel = cases.select(kind, params, "nominal")
+    L = binding.make_launch(kind, params, sel.applied)
+    narrow = _lib.jacobi_narrow(L, _dev(torch, init).data_ptr())
+    assert narrow
+    L.flags |= _lib.FLAG_NARROW
+
+    def sweep(src, dst, lo, hi):
+        _lib.jacobi_sweep(L, src.data_ptr(), dst.data_ptr(), lo, hi,
+                          torch.cuda.current_stream().cuda_stream)
+
+    box = {}
+    bufs = [_dev(torch, init) for _ in range(world)]
+    exs = [partition.LocalExchanger(r, world, box) for r in range(world)]
+    gens = [partition.run_stencil(family, params, bufs[r], exs[r], sweep, width=3) for r in range(world)]
+    partition.drive_local(gens)
+    torch.cuda.synchronize()
+    got = init.copy()
+    row = 1 if family == "jacobi" else N
+    half = N * row
+    for r in range(world):
+        lo, hi = partition.split(family, params, r, world)
+        b = bufs[r].cpu().numpy()
+        for off in (0, half):
+            got[off + lo * row: off + hi * row] = b[off + lo * row: off + hi * row]
+    assert np.array_equal(got, want)
+
+
+def test_wide_path_for_large_values(cuda, oracle_mod):
+    """Values beyond the narrow bound force 64-bit sums; results stay exact."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    N = 4098
+    rng = np.random.default_rng(2)
+    a = rng.integers(-(2**31), 2**31 - 1, size=2 * N).astype(np.int32)
+    params = {"T": 6, "N": N, "s": 4, "B": 64}
+    got = run_program(programs.source("jacobi"), params, {"a": a})["a"]
+    want = oracle_mod.run("jacobi", params, {"a": a})["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+    N2 = 66
+    a2 = rng.integers(-(2**31), 2**31 - 1, size=(2 * N2, N2)).astype(np.int32)
+    p2 = {"T": 4, "N": N2, "s": 2, "B0": 4, "B1": 8}
+    got = run_program(programs.source("jacobi2d"), p2, {"a": a2})["a"]
+    want = oracle_mod.run("jacobi2d", p2, {"a": a2})["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
