@@ -21,12 +21,17 @@
 // fit in int32.  A device-side pre-pass checks that bound once per run and
 // sets a flag the sweep kernels read (no host round trip); otherwise they
 // form 64-bit sums.  Both paths give identical results -- the 32-bit one
-// needs about a third of the integer instructions, which is what keeps the
-// sweeps memory-bound on B200.
+// needs about a third of the integer instructions.
 //
-// Tiles are aligned to even positions (columns) so every global access is
-// a 64-bit vector access in both halves (N may be = 2 mod 4, which rules
-// out 128-bit alignment of the upper half).
+// Staged tiles (cache(a) kept).  A block's window is copied to shared
+// memory with unguarded, batched 64-bit loads (the interior-tile test is
+// block-uniform, so only the first / last tiles take the guarded path),
+// laid out so the tile's first position sits on a 16-byte boundary.  Each
+// thread then computes four consecutive outputs from one 128-bit shared
+// load; the left / right neighbours come from the adjacent lanes by warp
+// shuffle (shared memory only at warp and row edges), and results leave as
+// two 64-bit stores.  64-bit (not 128-bit) global granularity because the
+// upper half starts at a + N and N = 2^28 + 2 is only 8-byte aligned.
 #include "pk_internal.cuh"
 
 namespace pk {
@@ -34,6 +39,7 @@ namespace {
 
 constexpr int kBound3 = 715827882;  // (2^31 - 1) / 3
 constexpr int kBound5 = 429496729;  // (2^31 - 1) / 5
+constexpr int kBatch = 4;           // independent 64-bit loads in flight per thread
 
 template <bool WIDE>
 __device__ __forceinline__ int avg3(int a, int b, int c) {
@@ -46,7 +52,7 @@ __device__ __forceinline__ int avg5(int a, int b, int c, int d, int e) {
     return (a + b + c + d + e) / 5;
 }
 
-// flag = 1 if every |v| <= bound over a[0, n), else 0 (flag preset to 1).
+// flag = 1 if every |v| <= bound over a[0, n), else 0 (flag preset non-zero).
 __global__ void __launch_bounds__(256) k_range_flag(const int *__restrict__ a, int64_t n, int bound,
                                                    int *__restrict__ flag) {
     bool ok = true;
@@ -67,43 +73,144 @@ __device__ __forceinline__ bool narrow_mode(int mode, const int *flag) {
     return mode == 2 ? (*flag != 0) : (mode == 1);
 }
 
+__device__ __forceinline__ void store4(int *dst, int64_t x, int64_t lo, int64_t hi, bool vec, int v0,
+                                       int v1, int v2, int v3) {
+    if (vec && x >= lo && x + 3 < hi) {
+        *reinterpret_cast<int2 *>(dst + x) = make_int2(v0, v1);
+        *reinterpret_cast<int2 *>(dst + x + 2) = make_int2(v2, v3);
+    } else {
+        if (x >= lo && x < hi) dst[x] = v0;
+        if (x + 1 >= lo && x + 1 < hi) dst[x + 1] = v1;
+        if (x + 2 >= lo && x + 2 < hi) dst[x + 2] = v2;
+        if (x + 3 >= lo && x + 3 < hi) dst[x + 3] = v3;
+    }
+}
+
 // ---------------------------------------------------------------- 1-D ------
 
-// Staged (cache(a) kept): the block's window src[xs-2, xs+tile+2) is copied
-// to shared memory with 64-bit loads, then each thread produces output pairs
-// (x, x+1) from it and stores them with one 64-bit store.
+// Outputs x = xs + 4p .. +3 from a shared window whose index 0 holds
+// position xs - 4 (sb is 16-byte aligned when al16, else 8-byte aligned).
+template <bool WIDE>
+__device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__restrict__ dst, int64_t lo,
+                                           int64_t hi, int64_t xs, int tile, bool vec) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int wlanes = min(32, nt - (tid - lane));  // lanes of this (possibly partial) warp
+    const unsigned wmask = wlanes == 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
+    const int quads = tile >> 2;
+    for (int pb = tid - lane; pb < quads; pb += nt) {  // warp-uniform trip count (shuffles)
+        const int p = pb + lane;
+        const bool act = p < quads;
+        int4 c = make_int4(0, 0, 0, 0);  // src[x .. x+3]
+        if (act) {
+            const int *q = sb + 4 * p + 4;
+            if (al16) {
+                c = *reinterpret_cast<const int4 *>(q);
+            } else {
+                const int2 u = *reinterpret_cast<const int2 *>(q), w = *reinterpret_cast<const int2 *>(q + 2);
+                c = make_int4(u.x, u.y, w.x, w.y);
+            }
+        }
+        int l = __shfl_up_sync(wmask, c.w, 1);
+        int r = __shfl_down_sync(wmask, c.x, 1);
+        if (!act) continue;
+        if (lane == 0) l = sb[4 * p + 3];
+        if (lane + 1 == wlanes || p + 1 == quads) r = sb[4 * p + 8];
+        const int64_t x = xs + 4 * (int64_t)p;
+        if (x + 3 < lo || x >= hi) continue;
+        store4(dst, x, lo, hi, vec, avg3<WIDE>(l, c.x, c.y), avg3<WIDE>(c.x, c.y, c.z),
+               avg3<WIDE>(c.y, c.z, c.w), avg3<WIDE>(c.z, c.w, r));
+    }
+}
+
+// Persistent TMA pipeline for interior tiles (whole window inside the
+// half): each block walks tiles t_begin + blockIdx.x + k*gridDim.x; one
+// thread issues a cp.async.bulk of tile k+1's window into the other shared
+// buffer while the block computes tile k, completion tracked by one
+// mbarrier per buffer.  The window start is rounded down to 16 bytes (TMA
+// alignment); its 8-byte remainder is the per-tile shift.
+constexpr int kTmaPad = 16;  // words of slack per buffer for the alignment shift
+
+template <bool WIDE>
+__device__ __forceinline__ void j1_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t lo,
+                                            int64_t hi, int64_t x0, int tile, int64_t t, int64_t t_end,
+                                            uint64_t *bar, int *bufs, int64_t t_stride) {
+    const int BW = tile + kTmaPad;
+    for (int k = 0; t < t_end; k++, t += t_stride) {
+        const int b = k & 1;
+        const int64_t tn = t + t_stride;
+        if (threadIdx.x == 0 && tn < t_end) {
+            fence_proxy_async();
+            const int *g = src + (x0 + tn * tile) - 4;
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
+            const int shift = (int)((ga & 15) >> 2);
+            const uint32_t bytes = (uint32_t)(((tile + 8 + shift) * 4 + 15) & ~15);
+            mbar_expect_tx(&bar[b ^ 1], bytes);
+            tma_load_1d(bufs + (b ^ 1) * BW, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes,
+                        &bar[b ^ 1]);
+        }
+        mbar_wait(&bar[b], (k >> 1) & 1);
+        const int64_t xs = x0 + t * tile;
+        const int shift = (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2);
+        j1_compute<WIDE>(bufs + b * BW + shift, shift == 0, dst, lo, hi, xs, tile, true);
+        __syncthreads();  // buffer b is refilled at iteration k+1
+    }
+}
+
+__global__ void __launch_bounds__(256) k_jacobi1d_tma(const int *__restrict__ src, int *__restrict__ dst,
+                                                     int64_t lo, int64_t hi, int64_t x0, int tile,
+                                                     int64_t t_begin, int64_t t_end, const int *flag,
+                                                     int mode) {
+    extern __shared__ __align__(128) int smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    int *bufs = smem + 8;  // 32-byte header: two mbarriers
+    const int64_t t = t_begin + blockIdx.x;
+    if (t >= t_end) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        const int *g = src + (x0 + t * tile) - 4;
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
+        const int shift = (int)((ga & 15) >> 2);
+        const uint32_t bytes = (uint32_t)(((tile + 8 + shift) * 4 + 15) & ~15);
+        mbar_expect_tx(&bar[0], bytes);
+        tma_load_1d(bufs, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, &bar[0]);
+    }
+    __syncthreads();
+    if (narrow_mode(mode, flag))
+        j1_tma_loop<false>(src, dst, lo, hi, x0, tile, t, t_end, bar, bufs, gridDim.x);
+    else
+        j1_tma_loop<true>(src, dst, lo, hi, x0, tile, t, t_end, bar, bufs, gridDim.x);
+}
+
+// window: positions [xs-4, xs+tile+4) at shared index pos - xs + 4 (tile % 4 == 0)
 template <bool WIDE>
 __device__ __forceinline__ void j1_staged_body(const int *__restrict__ src, int *__restrict__ dst,
                                                int64_t lo, int64_t hi, int64_t xs, int tile,
                                                int64_t limit, bool vec, int *sh) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int w2 = (tile + 8) >> 1;
     int2 *sh2 = reinterpret_cast<int2 *>(sh);
-    const int w2 = (tile + 4) >> 1;
-#pragma unroll 4
-    for (int q = tid; q < w2; q += nt) {
-        const int64_t i = xs - 2 + 2 * (int64_t)q;
-        if (vec && i >= 0 && i + 1 < limit) {
-            sh2[q] = *reinterpret_cast<const int2 *>(src + i);
-        } else {
-            sh[2 * q] = (i >= 0 && i < limit) ? src[i] : 0;
-            sh[2 * q + 1] = (i + 1 >= 0 && i + 1 < limit) ? src[i + 1] : 0;
+    const bool interior = vec && xs - 4 >= 0 && xs + tile + 4 <= limit;
+    if (interior) {
+        const int2 *g2 = reinterpret_cast<const int2 *>(src + xs - 4);
+        for (int q = tid; q < w2; q += kBatch * nt) {
+            int2 v[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++)
+                if (q + u * nt < w2) v[u] = g2[q + u * nt];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++)
+                if (q + u * nt < w2) sh2[q + u * nt] = v[u];
+        }
+    } else {
+        for (int q = tid; q < 2 * w2; q += nt) {
+            const int64_t i = xs - 4 + q;
+            sh[q] = (i >= 0 && i < limit) ? src[i] : 0;
         }
     }
     __syncthreads();
-    const int pairs = tile >> 1;
-#pragma unroll 4
-    for (int p = tid; p < pairs; p += nt) {
-        const int64_t x = xs + 2 * (int64_t)p;
-        const int2 c = sh2[p + 1];  // src[x], src[x+1]
-        const int l = sh[2 * p + 1], r = sh[2 * p + 4];
-        const int v0 = avg3<WIDE>(l, c.x, c.y), v1 = avg3<WIDE>(c.x, c.y, r);
-        if (vec && x >= lo && x + 1 < hi) {
-            *reinterpret_cast<int2 *>(dst + x) = make_int2(v0, v1);
-        } else {
-            if (x >= lo && x < hi) dst[x] = v0;
-            if (x + 1 >= lo && x + 1 < hi) dst[x + 1] = v1;
-        }
-    }
+    j1_compute<WIDE>(sh, true, dst, lo, hi, xs, tile, vec);
 }
 
 __global__ void __launch_bounds__(1024) k_jacobi1d_staged(const int *__restrict__ src,
@@ -125,20 +232,24 @@ template <bool WIDE>
 __device__ __forceinline__ void j1_direct_body(const int *__restrict__ src, int *__restrict__ dst,
                                                int64_t lo, int64_t hi, int64_t xs, int tile, bool vec) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int pairs = tile >> 1;
-#pragma unroll 4
-    for (int p = tid; p < pairs; p += nt) {
-        const int64_t x = xs + 2 * (int64_t)p;
-        if (x + 1 < lo || x >= hi) continue;
-        const int2 c = vec ? *reinterpret_cast<const int2 *>(src + x) : make_int2(src[x], src[x + 1]);
-        const int l = src[x - 1], r = src[x + 2];
-        const int v0 = avg3<WIDE>(l, c.x, c.y), v1 = avg3<WIDE>(c.x, c.y, r);
-        if (vec && x >= lo && x + 1 < hi) {
-            *reinterpret_cast<int2 *>(dst + x) = make_int2(v0, v1);
+    const int quads = tile >> 2;
+#pragma unroll 2
+    for (int p = tid; p < quads; p += nt) {
+        const int64_t x = xs + 4 * (int64_t)p;
+        if (x + 3 < lo || x >= hi) continue;
+        // read only what a written output needs: x-1 >= lo-1 >= 0 and x+4 <= hi <= N-1
+        const int l = x >= lo ? src[x - 1] : 0;
+        const int r = x + 3 < hi ? src[x + 4] : 0;
+        int2 c0, c1;
+        if (vec && x >= lo && x + 3 < hi) {
+            c0 = *reinterpret_cast<const int2 *>(src + x);
+            c1 = *reinterpret_cast<const int2 *>(src + x + 2);
         } else {
-            if (x >= lo && x < hi) dst[x] = v0;
-            if (x + 1 >= lo && x + 1 < hi) dst[x + 1] = v1;
+            c0 = make_int2(src[x], x + 1 <= hi ? src[x + 1] : 0);
+            c1 = make_int2(x + 2 <= hi ? src[x + 2] : 0, x + 3 <= hi ? src[x + 3] : 0);
         }
+        store4(dst, x, lo, hi, vec, avg3<WIDE>(l, c0.x, c0.y), avg3<WIDE>(c0.x, c0.y, c1.x),
+               avg3<WIDE>(c0.y, c1.x, c1.y), avg3<WIDE>(c1.x, c1.y, r));
     }
 }
 
@@ -155,117 +266,273 @@ __global__ void __launch_bounds__(1024) k_jacobi1d_direct(const int *__restrict_
 
 // ---------------------------------------------------------------- 2-D ------
 
-// Staged: the (TI+2) x (TJ+4) window (rows r0-1..r0+TI, cols c0-2..c0+TJ+1)
-// is copied to shared memory (64-bit loads when N is even); each thread then
-// owns a column pair and marches down its rows keeping the up/centre/down
-// values in registers, so a row costs one 64-bit and two 32-bit shared
-// loads per two outputs.
+// Window: rows r0-1 .. r0+nr, columns c0-4 .. c0+TJ+3 (pitch TJ+8), column j
+// at shared index j - c0 + 4.  Each thread owns a column quad and marches
+// down its row group keeping the rows above / at / below in registers: one
+// 128-bit shared load per row per four outputs.
+//
+// j2_compute reads window row rr at base + rr*pitch + shift(rr), shift(rr) =
+// (s0 + rr*ds) & 3 in {0, 2} words (TMA rows start on 16 bytes; rows of an
+// N = 2 mod 4 matrix alternate between the two alignments).
+__device__ __forceinline__ int4 lds4(const int *p, bool al16) {
+    if (al16) return *reinterpret_cast<const int4 *>(p);
+    const int2 u = *reinterpret_cast<const int2 *>(p), w = *reinterpret_cast<const int2 *>(p + 2);
+    return make_int4(u.x, u.y, w.x, w.y);
+}
+
+// Per-thread role in a TI x TJ tile, fixed for the whole kernel: column
+// quad qd of row group g (groups of nq = TJ/4 threads march rpg rows each).
+struct J2Role {
+    int qd, rb, rpg, passes, lc;
+    bool act, lin, rin;
+    unsigned wmask;
+};
+
+__device__ __forceinline__ J2Role j2_role(int TI, int TJ, int qb) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int nq = TJ >> 2;
+    J2Role r;
+    const int groups = nt >= nq ? nt / nq : 1;
+    r.passes = nt >= nq ? 1 : (nq + nt - 1) / nt;
+    r.rpg = (TI + groups - 1) / groups;
+    r.qd = nt >= nq ? tid % nq : tid + qb * nt;
+    const int g = nt >= nq ? tid / nq : 0;
+    r.act = g < groups && r.qd < nq;
+    r.rb = g * r.rpg;
+    r.lc = 4 * r.qd + 4;
+    const int wlanes = min(32, nt - (tid - lane));
+    r.wmask = wlanes == 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
+    r.lin = lane > 0 && r.qd > 0;
+    r.rin = lane + 1 < wlanes && r.qd + 1 < nq;
+    return r;
+}
+
+// One role's column quad over its rows of the tile at (r0, c0): drow points
+// at dst row r0, columns relative to c0.
+template <bool WIDE>
+__device__ __forceinline__ void j2_march(const J2Role &R, const int *base, int pitch, int s0, int ds,
+                                         int *__restrict__ drow, int64_t N, int nr, int64_t c0, int64_t J,
+                                         bool vec) {
+    const int64_t j = c0 + 4 * (int64_t)R.qd;  // output columns j .. j+3
+    int sh = (s0 + R.rb * ds) & 3;             // alignment shift of window row rb
+    const int *p = base + R.rb * pitch + sh + R.lc;
+    int4 up = make_int4(0, 0, 0, 0), cur = up;
+    const bool go = R.act && R.rb < nr;
+    if (go) up = lds4(p, sh == 0);
+    p += pitch - sh;
+    sh = (sh + ds) & 3;
+    p += sh;
+    if (go) cur = lds4(p, sh == 0);
+    int *o = drow + (int64_t)R.rb * N + 4 * R.qd;
+    for (int k = 0; k < R.rpg; k++) {  // warp-uniform trip count (shuffles)
+        const int *crow = p;
+        const bool live = R.act && R.rb + k < nr;
+        p += pitch - sh;
+        sh = (sh + ds) & 3;
+        p += sh;
+        const int4 dn = live ? lds4(p, sh == 0) : make_int4(0, 0, 0, 0);
+        int l = __shfl_up_sync(R.wmask, cur.w, 1);
+        int r = __shfl_down_sync(R.wmask, cur.x, 1);
+        if (live) {
+            if (!R.lin) l = crow[-1];
+            if (!R.rin) r = crow[4];
+            const int v0 = avg5<WIDE>(up.x, dn.x, l, cur.y, cur.x);
+            const int v1 = avg5<WIDE>(up.y, dn.y, cur.x, cur.z, cur.y);
+            const int v2 = avg5<WIDE>(up.z, dn.z, cur.y, cur.w, cur.z);
+            const int v3 = avg5<WIDE>(up.w, dn.w, cur.z, r, cur.w);
+            store4(o - j, j, 1, J + 1, vec, v0, v1, v2, v3);
+        }
+        o += N;
+        up = cur;
+        cur = dn;
+    }
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void j2_compute(const int *base, int pitch, int s0, int ds, int *__restrict__ dst,
+                                           int64_t N, int64_t r0, int nr, int64_t c0, int64_t J, int TI, int TJ,
+                                           bool vec) {
+    const int passes = j2_role(TI, TJ, 0).passes;
+    for (int qb = 0; qb < passes; qb++)
+        j2_march<WIDE>(j2_role(TI, TJ, qb), base, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, vec);
+}
+
+// Persistent TMA pipeline for interior 2-D tiles: warp 0 issues one bulk
+// copy per window row (rows start on 16-byte boundaries; the remainder is
+// the row's shift) into the buffer not being computed on.
+constexpr int kRowPad = 16;  // words of slack per window row for the alignment shift
+
+__device__ __forceinline__ void j2_issue(const int *src, int64_t N, int64_t r0, int nr, int64_t c0, int TJ,
+                                         int *buf, int pitch, uint64_t *bar) {
+    const int lane = threadIdx.x & 31;
+    const int rows = nr + 2;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
+    const int s0 = (int)((a0 & 15) >> 2), ds = (int)(N & 3);
+    if (lane == 0) {
+        uint32_t total = 0;
+        for (int rr = 0; rr < rows; rr++) total += (uint32_t)(((TJ + 8 + ((s0 + rr * ds) & 3)) * 4 + 15) & ~15);
+        mbar_expect_tx(bar, total);
+    }
+    __syncwarp();
+    for (int rr = lane; rr < rows; rr += 32) {
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (r0 - 1 + rr) * N + c0 - 4);
+        const int sh = (int)((ga & 15) >> 2);
+        const uint32_t bytes = (uint32_t)(((TJ + 8 + sh) * 4 + 15) & ~15);
+        tma_load_1d(buf + rr * pitch, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, bar);
+    }
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t N,
+                                            int64_t rlo, int64_t rhi, int64_t J, int TI, int TJ, int64_t tc0,
+                                            int64_t ntc, int64_t t, int64_t t_end, uint64_t *bar, int *bufs,
+                                            bool vec) {
+    const int pitch = TJ + kRowPad;
+    const int BW = (TI + 2) * pitch;
+    const J2Role role = j2_role(TI, TJ, 0);  // fixed for every tile of this block
+    const uint32_t ntc32 = (uint32_t)ntc;
+    uint32_t tr = (uint32_t)t / ntc32, tc = (uint32_t)t - tr * ntc32;  // tile -> (row tile, column tile)
+    const uint32_t str = (uint32_t)gridDim.x / ntc32, stc = (uint32_t)gridDim.x - str * ntc32;
+    for (int k = 0; t < t_end; k++, t += gridDim.x) {
+        const int b = k & 1;
+        const int64_t tn = t + gridDim.x;
+        uint32_t trn = tr + str, tcn = tc + stc;
+        if (tcn >= ntc32) {
+            tcn -= ntc32;
+            trn++;
+        }
+        if (threadIdx.x < 32 && tn < t_end) {
+            fence_proxy_async();  // every issuing lane orders the block's earlier reads
+            __syncwarp();
+            const int64_t r0n = rlo + (int64_t)trn * TI, c0n = (tc0 + tcn) * (int64_t)TJ;
+            j2_issue(src, N, r0n, (int)min((int64_t)TI, rhi - r0n), c0n, TJ, bufs + (b ^ 1) * BW, pitch,
+                     &bar[b ^ 1]);
+        }
+        mbar_wait(&bar[b], (k >> 1) & 1);
+        const int64_t r0 = rlo + (int64_t)tr * TI, c0 = (tc0 + tc) * (int64_t)TJ;
+        const int nr = (int)min((int64_t)TI, rhi - r0);
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
+        const int s0 = (int)((a0 & 15) >> 2), ds = (int)(N & 3);
+        if (role.passes == 1)
+            j2_march<WIDE>(role, bufs + b * BW, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, vec);
+        else
+            j2_compute<WIDE>(bufs + b * BW, pitch, s0, ds, dst, N, r0, nr, c0, J, TI, TJ, vec);
+        tr = trn;
+        tc = tcn;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ src, int *__restrict__ dst,
+                                                      int64_t N, int64_t rlo, int64_t rhi, int64_t J, int TI,
+                                                      int TJ, int64_t tc0, int64_t ntc, int64_t ntiles,
+                                                      const int *flag, int mode) {
+    extern __shared__ __align__(128) int smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    int *bufs = smem + 8;
+    const int64_t t = blockIdx.x;
+    if (t >= ntiles) return;
+    const int pitch = TJ + kRowPad;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int64_t r0 = rlo + (t / ntc) * TI, c0 = (tc0 + t % ntc) * TJ;
+        j2_issue(src, N, r0, (int)min((int64_t)TI, rhi - r0), c0, TJ, bufs, pitch, &bar[0]);
+    }
+    if (narrow_mode(mode, flag))
+        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, tc0, ntc, t, ntiles, bar, bufs, true);
+    else
+        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, tc0, ntc, t, ntiles, bar, bufs, true);
+}
+
 template <bool WIDE>
 __device__ __forceinline__ void j2_staged_body(const int *__restrict__ src, int *__restrict__ dst,
                                                int64_t N, int64_t r0, int64_t rhi, int64_t c0,
                                                int64_t J, int TI, int TJ, bool vec, int *sh) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int pitch = TJ + 4;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int pitch = TJ + 8, w2 = pitch >> 1;
     const int nr = (int)min((int64_t)TI, rhi - r0);
-    // ---- load window
-    const int w2 = pitch >> 1;
-    for (int e = tid; e < (nr + 2) * w2; e += nt) {
-        const int rr = e / w2, q = e - rr * w2;
-        const int64_t row = r0 - 1 + rr;
-        const int64_t col = c0 - 2 + 2 * (int64_t)q;
-        const int *s = src + row * N + col;
-        int *d = sh + rr * pitch + 2 * q;
-        if (vec && col >= 0 && col + 1 < N) {
-            *reinterpret_cast<int2 *>(d) = *reinterpret_cast<const int2 *>(s);
-        } else {
-            d[0] = (col >= 0 && col < N) ? s[0] : 0;
-            d[1] = (col + 1 >= 0 && col + 1 < N) ? s[1] : 0;
+    const int rows = nr + 2;
+    const bool interior = vec && c0 - 4 >= 0 && c0 + TJ + 4 <= N;
+    if (interior) {
+        // batched, unguarded: element e = (row, q) advanced by nt per step
+        const int drow = nt / w2, dq = nt - drow * w2;
+        int row = tid / w2, q = tid - row * w2;
+        const int2 *g0 = reinterpret_cast<const int2 *>(src + (r0 - 1) * N + c0 - 4);
+        const int64_t rstride2 = N >> 1;  // N even on this path
+        while (row < rows) {
+            int2 v[kBatch];
+            int rr[kBatch], qq[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; u++) {
+                rr[u] = row;
+                qq[u] = q;
+                if (row < rows) v[u] = g0[(int64_t)row * rstride2 + q];
+                row += drow;
+                q += dq;
+                if (q >= w2) {
+                    q -= w2;
+                    row++;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; u++)
+                if (rr[u] < rows) reinterpret_cast<int2 *>(sh + rr[u] * pitch)[qq[u]] = v[u];
+        }
+    } else {
+        for (int e = tid; e < rows * pitch; e += nt) {
+            const int rr = e / pitch, cc = e - rr * pitch;
+            const int64_t col = c0 - 4 + cc;
+            sh[e] = (col >= 0 && col < N) ? src[(r0 - 1 + rr) * N + col] : 0;
         }
     }
     __syncthreads();
-    // ---- compute: thread -> (column pair, row group)
-    const int ncp = TJ >> 1;
-    auto march = [&](int cp, int rb, int re) {
-        const int64_t j = c0 + 2 * (int64_t)cp;  // output columns j, j+1
-        const bool in0 = j >= 1 && j <= J, in1 = j + 1 >= 1 && j + 1 <= J;
-        if ((!in0 && !in1) || rb >= re) return;
-        const int lc = 2 * cp + 2;  // window column of j
-        int2 up = *reinterpret_cast<const int2 *>(sh + rb * pitch + lc);
-        int2 cur = *reinterpret_cast<const int2 *>(sh + (rb + 1) * pitch + lc);
-        for (int rr = rb; rr < re; rr++) {
-            const int *crow = sh + (rr + 1) * pitch + lc;
-            const int2 dn = *reinterpret_cast<const int2 *>(crow + pitch);
-            const int l = crow[-1], r = crow[2];
-            const int v0 = avg5<WIDE>(up.x, dn.x, l, cur.y, cur.x);
-            const int v1 = avg5<WIDE>(up.y, dn.y, cur.x, r, cur.y);
-            int *o = dst + (r0 + rr) * N + j;
-            if (in0 && in1 && vec) {
-                *reinterpret_cast<int2 *>(o) = make_int2(v0, v1);
-            } else {
-                if (in0) o[0] = v0;
-                if (in1) o[1] = v1;
-            }
-            up = cur;
-            cur = dn;
-        }
-    };
-    if (nt >= ncp) {
-        const int groups = nt / ncp, g = tid / ncp;
-        const int rpg = (nr + groups - 1) / groups;
-        if (g < groups) march(tid % ncp, g * rpg, min(nr, (g + 1) * rpg));
-    } else {
-        for (int cp = tid; cp < ncp; cp += nt) march(cp, 0, nr);
-    }
+    (void)lane;
+    j2_compute<WIDE>(sh, pitch, 0, 0, dst, N, r0, nr, c0, J, TI, TJ, vec);
 }
 
 __global__ void __launch_bounds__(1024) k_jacobi2d_staged(const int *__restrict__ src,
                                                          int *__restrict__ dst, int64_t N,
                                                          int64_t rlo, int64_t rhi, int64_t J,
-                                                         int TI, int TJ, int64_t ntj, int vec,
+                                                         int TI, int TJ, int64_t tc0, int64_t ntj, int vec,
                                                          const int *flag, int mode) {
     extern __shared__ __align__(16) int sh[];
     const int64_t bid = blockIdx.x;
-    const int64_t r0 = rlo + (bid / ntj) * TI, c0 = (bid % ntj) * TJ;
+    const int64_t r0 = rlo + (bid / ntj) * TI, c0 = (tc0 + bid % ntj) * TJ;
     if (narrow_mode(mode, flag))
         j2_staged_body<false>(src, dst, N, r0, rhi, c0, J, TI, TJ, vec != 0, sh);
     else
         j2_staged_body<true>(src, dst, N, r0, rhi, c0, J, TI, TJ, vec != 0, sh);
 }
 
-// caching-off: a thread owns a column pair of TI rows and reads the five
-// neighbours from global memory (row above / below through L1/L2).
+// caching-off: a thread owns a column quad of one row and reads the five
+// neighbours from global memory (rows above / below through L1/L2).
 template <bool WIDE>
 __device__ __forceinline__ void j2_direct_body(const int *__restrict__ src, int *__restrict__ dst,
                                                int64_t N, int64_t r0, int64_t rhi, int64_t c0,
                                                int64_t J, int TI, int TJ, bool vec) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int nr = (int)min((int64_t)TI, rhi - r0);
-    const int ncp = TJ >> 1;
-    for (int e = tid; e < nr * ncp; e += nt) {
-        const int rr = e / ncp, cp = e - rr * ncp;
-        const int64_t i = r0 + rr, j = c0 + 2 * (int64_t)cp;
-        const bool in0 = j >= 1 && j <= J, in1 = j + 1 >= 1 && j + 1 <= J;
-        if (!in0 && !in1) continue;
-        const int *m = src + i * N + j;
-        int2 c, u, d;
-        if (vec) {
-            c = *reinterpret_cast<const int2 *>(m);
-            u = *reinterpret_cast<const int2 *>(m - N);
-            d = *reinterpret_cast<const int2 *>(m + N);
-        } else {
-            c = make_int2(m[0], m[1]);
-            u = make_int2(m[-N], m[1 - N]);
-            d = make_int2(m[N], m[1 + N]);
+    const int nq = TJ >> 2;
+    for (int e = tid; e < nr * nq; e += nt) {
+        const int rr = e / nq, qd = e - rr * nq;
+        const int64_t i = r0 + rr, j = c0 + 4 * (int64_t)qd;
+        if (j + 3 < 1 || j > J) continue;
+        const int *m = src + i * N;
+        int v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int64_t jj = j + k;
+            if (jj >= 1 && jj <= J)
+                v[k] = avg5<WIDE>(m[jj - N], m[jj + N], m[jj - 1], m[jj + 1], m[jj]);
+            else
+                v[k] = 0;
         }
-        const int l = m[-1], r = m[2];
-        const int v0 = avg5<WIDE>(u.x, d.x, l, c.y, c.x), v1 = avg5<WIDE>(u.y, d.y, c.x, r, c.y);
-        int *o = dst + i * N + j;
-        if (in0 && in1 && vec) {
-            *reinterpret_cast<int2 *>(o) = make_int2(v0, v1);
-        } else {
-            if (in0) o[0] = v0;
-            if (in1) o[1] = v1;
-        }
+        store4(dst + i * N, j, 1, J + 1, vec, v[0], v[1], v[2], v[3]);
     }
 }
 
@@ -314,6 +581,8 @@ int sweep_mode(const pk_launch_t &L, const int *flag) {
     return (L.flags & PK_FLAG_NARROW) ? 1 : 0;
 }
 
+inline int64_t round4(int64_t v) { return (v + 3) & ~(int64_t)3; }
+
 int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int64_t hi,
                  const int *flag, cudaStream_t st) {
     Extents1D e;
@@ -322,9 +591,9 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     if (lo < 1) lo = 1;
     if (hi > e.P + 1) hi = e.P + 1;
     if (hi <= lo) return PK_OK;
-    int64_t tile64 = elems(L) * L.B;
-    if (tile64 & 1) tile64 += 1;  // the pair layout needs an even tile; coverage is unchanged
-    if (tile64 > (1 << 30)) return fail(PK_E_UNSUPPORTED, "jacobi: tile too large");
+    // the quad layout needs tile % 4 == 0; coverage comes from [lo, hi), not the tile
+    const int64_t tile64 = round4(elems(L) * L.B);
+    if (tile64 > (1 << 28)) return fail(PK_E_UNSUPPORTED, "jacobi: tile too large");
     const int tile = (int)tile64;
     const int nt = (int)(L.B < 1024 ? L.B : 1024);
     const int64_t x0 = lo & ~(int64_t)1;
@@ -333,13 +602,44 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     const int vec = !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7u);
     const int mode = sweep_mode(L, flag);
     if (L.variant == PK_VARIANT_STAGED) {
-        const size_t smem = ((size_t)tile + 4) * sizeof(int);
+        // tiles whose whole (16-byte rounded) window lies inside the half go
+        // through the TMA pipeline; the one or two edge tiles through the
+        // guarded kernel
+        int64_t ta = 0, tb = 0;
+        if (vec && tile >= 64 && tile <= 8192) {
+            ta = x0 >= 8 ? 0 : ceil_div(8 - x0, tile);
+            const int64_t room = L.N - 8 - tile - x0;
+            tb = room >= 0 ? room / tile + 1 : 0;
+            if (tb > blocks) tb = blocks;
+            if (tb - ta < 2) ta = tb = 0;
+        }
+        const size_t smem = ((size_t)tile + 8) * sizeof(int);
         rc = allow_smem((const void *)k_jacobi1d_staged, smem);
         if (rc) return rc;
-        k_jacobi1d_staged<<<(unsigned)blocks, nt, smem, st>>>(src, dst, lo, hi, x0, tile, L.N, vec, flag, mode);
-    } else {
-        k_jacobi1d_direct<<<(unsigned)blocks, nt, 0, st>>>(src, dst, lo, hi, x0, tile, vec, flag, mode);
+        auto generic = [&](int64_t t0, int64_t t1) -> int {
+            if (t1 <= t0) return PK_OK;
+            k_jacobi1d_staged<<<(unsigned)(t1 - t0), nt, smem, st>>>(src, dst, lo, hi, x0 + t0 * tile, tile,
+                                                                     L.N, vec, flag, mode);
+            return after_launch("jacobi1d");
+        };
+        if (tb > ta) {
+            if ((rc = generic(0, ta)) || (rc = generic(tb, blocks))) return rc;
+            const size_t tsmem = 32 + 2 * ((size_t)tile + kTmaPad) * sizeof(int);
+            rc = allow_smem((const void *)k_jacobi1d_tma, tsmem);
+            if (rc) return rc;
+            const int tnt = nt < 256 ? nt : 256;
+            int per_sm = 0, sms = 148, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi1d_tma, tnt, tsmem);
+            int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+            if (grid > tb - ta) grid = tb - ta;
+            k_jacobi1d_tma<<<(unsigned)grid, tnt, tsmem, st>>>(src, dst, lo, hi, x0, tile, ta, tb, flag, mode);
+            return after_launch("jacobi1d_tma");
+        }
+        return generic(0, blocks);
     }
+    k_jacobi1d_direct<<<(unsigned)blocks, nt, 0, st>>>(src, dst, lo, hi, x0, tile, vec, flag, mode);
     return after_launch("jacobi1d");
 }
 
@@ -351,8 +651,7 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     if (lo < 1) lo = 1;
     if (hi > e.I + 1) hi = e.I + 1;
     if (hi <= lo || e.J <= 0) return PK_OK;
-    int64_t TI64 = L.B0, TJ64 = elems(L) * L.B1;
-    if (TJ64 & 1) TJ64 += 1;
+    const int64_t TI64 = L.B0, TJ64 = round4(elems(L) * L.B1);
     if (TI64 * TJ64 > (1 << 26)) return fail(PK_E_UNSUPPORTED, "jacobi2d: tile too large");
     const int TI = (int)TI64, TJ = (int)TJ64;
     int64_t nthreads = L.B0 * L.B1;
@@ -363,11 +662,38 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     const int vec = (L.N % 2 == 0) && !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7u);
     const int mode = sweep_mode(L, flag);
     if (L.variant == PK_VARIANT_STAGED) {
-        const size_t smem = (size_t)(TI + 2) * (size_t)(TJ + 4) * sizeof(int);
+        const size_t smem = (size_t)(TI + 2) * (size_t)(TJ + 8) * sizeof(int);
         rc = allow_smem((const void *)k_jacobi2d_staged, smem);
         if (rc) return rc;
-        k_jacobi2d_staged<<<(unsigned)blocks, (unsigned)nthreads, smem, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ,
-                                                                              ntj, vec, flag, mode);
+        auto generic = [&](int64_t tc0, int64_t ntc) -> int {
+            if (ntc <= 0) return PK_OK;
+            k_jacobi2d_staged<<<(unsigned)(nti * ntc), (unsigned)nthreads, smem, st>>>(
+                src, dst, L.N, lo, hi, e.J, TI, TJ, tc0, ntc, vec, flag, mode);
+            return after_launch("jacobi2d");
+        };
+        // column tiles whose rounded window rows lie inside the matrix row
+        // take the TMA pipeline; the edge columns the guarded kernel
+        int64_t ca = (8 + TJ - 1) / TJ, cb = 0;
+        const int64_t room = L.N - 8 - TJ;
+        if (vec && nthreads % 32 == 0 && nthreads <= 512 && room >= 0) cb = room / TJ + 1;
+        if (cb > ntj) cb = ntj;
+        if (cb - ca >= 1) {
+            if ((rc = generic(0, ca)) || (rc = generic(cb, ntj - cb))) return rc;
+            const size_t tsmem = 32 + 2 * (size_t)(TI + 2) * (size_t)(TJ + kRowPad) * sizeof(int);
+            rc = allow_smem((const void *)k_jacobi2d_tma, tsmem);
+            if (rc) return rc;
+            int per_sm = 0, sms = 148, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi2d_tma, (int)nthreads, tsmem);
+            const int64_t ntiles = nti * (cb - ca);
+            int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+            if (grid > ntiles) grid = ntiles;
+            k_jacobi2d_tma<<<(unsigned)grid, (unsigned)nthreads, tsmem, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ,
+                                                                             ca, cb - ca, ntiles, flag, mode);
+            return after_launch("jacobi2d_tma");
+        }
+        return generic(0, ntj);
     } else {
         k_jacobi2d_direct<<<(unsigned)blocks, (unsigned)nthreads, 0, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ,
                                                                            ntj, vec, flag, mode);
@@ -375,7 +701,7 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     return after_launch("jacobi2d");
 }
 
-// Device flag: 1 when the whole double buffer is within the narrow bound.
+// Device flag: non-zero when the whole double buffer is within the narrow bound.
 int range_flag(const int *a, int64_t n, int bound, int **flag, cudaStream_t st) {
     cudaError_t err = cudaMallocAsync((void **)flag, sizeof(int), st);
     if (err != cudaSuccess) return fail(PK_E_ALLOC, "cudaMallocAsync(flag): %s", cudaGetErrorString(err));
@@ -411,6 +737,7 @@ int jacobi_narrow(const pk_launch_t &L, const void *a, int *narrow, cudaStream_t
     cudaFreeAsync(flag, st);
     cudaError_t err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) return fail(PK_E_CUDA, "range check: %s", cudaGetErrorString(err));
+    *narrow = *narrow != 0;
     return PK_OK;
 }
 
