@@ -130,57 +130,69 @@ __device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__rest
 // alignment); its 8-byte remainder is the per-tile shift.
 constexpr int kTmaPad = 16;  // words of slack per buffer for the alignment shift
 
+// Tiles [ta, tb) have their whole rounded window inside the half and are
+// TMA-fed; the edge tiles outside it (at most one or two per sweep) are
+// filled by guarded loads of the whole block, in turn, from the same loop.
+__device__ __forceinline__ void j1_issue(const int *src, int64_t xs, int tile, int *buf, uint64_t *bar) {
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(src + xs - 4);
+    const int shift = (int)((ga & 15) >> 2);
+    const uint32_t bytes = (uint32_t)(((tile + 8 + shift) * 4 + 15) & ~15);
+    mbar_expect_tx(bar, bytes);
+    tma_load_1d(buf, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, bar);
+}
+
 template <bool WIDE>
 __device__ __forceinline__ void j1_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t lo,
-                                            int64_t hi, int64_t x0, int tile, int64_t t, int64_t t_end,
-                                            uint64_t *bar, int *bufs, int64_t t_stride) {
+                                            int64_t hi, int64_t x0, int tile, int64_t t, int64_t ntiles,
+                                            int64_t ta, int64_t tb, int64_t limit, uint64_t *bar, int *bufs) {
     const int BW = tile + kTmaPad;
-    for (int k = 0; t < t_end; k++, t += t_stride) {
+    uint32_t fills[2] = {0u, 0u};  // completed TMA phases per buffer (block-uniform)
+    for (int k = 0; t < ntiles; k++, t += gridDim.x) {
         const int b = k & 1;
-        const int64_t tn = t + t_stride;
-        if (threadIdx.x == 0 && tn < t_end) {
+        const int64_t tn = t + gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles && tn >= ta && tn < tb) {
             fence_proxy_async();
-            const int *g = src + (x0 + tn * tile) - 4;
-            const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
-            const int shift = (int)((ga & 15) >> 2);
-            const uint32_t bytes = (uint32_t)(((tile + 8 + shift) * 4 + 15) & ~15);
-            mbar_expect_tx(&bar[b ^ 1], bytes);
-            tma_load_1d(bufs + (b ^ 1) * BW, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes,
-                        &bar[b ^ 1]);
+            j1_issue(src, x0 + tn * tile, tile, bufs + (b ^ 1) * BW, &bar[b ^ 1]);
         }
-        mbar_wait(&bar[b], (k >> 1) & 1);
         const int64_t xs = x0 + t * tile;
-        const int shift = (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2);
-        j1_compute<WIDE>(bufs + b * BW + shift, shift == 0, dst, lo, hi, xs, tile, true);
+        int *buf = bufs + b * BW;
+        int shift = 0;
+        if (t >= ta && t < tb) {
+            mbar_wait(&bar[b], fills[b] & 1);
+            fills[b]++;
+            shift = (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2);
+        } else {
+            for (int q = threadIdx.x; q < tile + 8; q += blockDim.x) {
+                const int64_t i = xs - 4 + q;
+                buf[q] = (i >= 0 && i < limit) ? src[i] : 0;
+            }
+            __syncthreads();
+        }
+        j1_compute<WIDE>(buf + shift, shift == 0, dst, lo, hi, xs, tile, true);
         __syncthreads();  // buffer b is refilled at iteration k+1
     }
 }
 
 __global__ void __launch_bounds__(256) k_jacobi1d_tma(const int *__restrict__ src, int *__restrict__ dst,
                                                      int64_t lo, int64_t hi, int64_t x0, int tile,
-                                                     int64_t t_begin, int64_t t_end, const int *flag,
-                                                     int mode) {
+                                                     int64_t ntiles, int64_t ta, int64_t tb, int64_t limit,
+                                                     const int *flag, int mode) {
     extern __shared__ __align__(128) int smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     int *bufs = smem + 8;  // 32-byte header: two mbarriers
-    const int64_t t = t_begin + blockIdx.x;
-    if (t >= t_end) return;
+    const int64_t t = blockIdx.x;
+    if (t >= ntiles) return;
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_mbar_init();
-        const int *g = src + (x0 + t * tile) - 4;
-        const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
-        const int shift = (int)((ga & 15) >> 2);
-        const uint32_t bytes = (uint32_t)(((tile + 8 + shift) * 4 + 15) & ~15);
-        mbar_expect_tx(&bar[0], bytes);
-        tma_load_1d(bufs, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, &bar[0]);
+        if (t >= ta && t < tb) j1_issue(src, x0 + t * tile, tile, bufs, &bar[0]);
     }
     __syncthreads();
     if (narrow_mode(mode, flag))
-        j1_tma_loop<false>(src, dst, lo, hi, x0, tile, t, t_end, bar, bufs, gridDim.x);
+        j1_tma_loop<false>(src, dst, lo, hi, x0, tile, t, ntiles, ta, tb, limit, bar, bufs);
     else
-        j1_tma_loop<true>(src, dst, lo, hi, x0, tile, t, t_end, bar, bufs, gridDim.x);
+        j1_tma_loop<true>(src, dst, lo, hi, x0, tile, t, ntiles, ta, tb, limit, bar, bufs);
 }
 
 // window: positions [xs-4, xs+tile+4) at shared index pos - xs + 4 (tile % 4 == 0)
@@ -382,17 +394,21 @@ __device__ __forceinline__ void j2_issue(const int *src, int64_t N, int64_t r0, 
     }
 }
 
+// Column tiles [ca, cb) are TMA-fed; the edge columns (whose rounded
+// window rows would leave the matrix row) are filled by guarded loads of
+// the whole block from the same persistent loop.
 template <bool WIDE>
 __device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t N,
-                                            int64_t rlo, int64_t rhi, int64_t J, int TI, int TJ, int64_t tc0,
-                                            int64_t ntc, int64_t t, int64_t t_end, uint64_t *bar, int *bufs,
-                                            bool vec) {
+                                            int64_t rlo, int64_t rhi, int64_t J, int TI, int TJ, int64_t ntc,
+                                            int64_t ca, int64_t cb, int64_t t, int64_t t_end, uint64_t *bar,
+                                            int *bufs) {
     const int pitch = TJ + kRowPad;
     const int BW = (TI + 2) * pitch;
     const J2Role role = j2_role(TI, TJ, 0);  // fixed for every tile of this block
     const uint32_t ntc32 = (uint32_t)ntc;
     uint32_t tr = (uint32_t)t / ntc32, tc = (uint32_t)t - tr * ntc32;  // tile -> (row tile, column tile)
     const uint32_t str = (uint32_t)gridDim.x / ntc32, stc = (uint32_t)gridDim.x - str * ntc32;
+    uint32_t fills[2] = {0u, 0u};  // completed TMA phases per buffer (block-uniform)
     for (int k = 0; t < t_end; k++, t += gridDim.x) {
         const int b = k & 1;
         const int64_t tn = t + gridDim.x;
@@ -401,22 +417,35 @@ __device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__
             tcn -= ntc32;
             trn++;
         }
-        if (threadIdx.x < 32 && tn < t_end) {
+        if (threadIdx.x < 32 && tn < t_end && tcn >= ca && tcn < cb) {
             fence_proxy_async();  // every issuing lane orders the block's earlier reads
             __syncwarp();
-            const int64_t r0n = rlo + (int64_t)trn * TI, c0n = (tc0 + tcn) * (int64_t)TJ;
+            const int64_t r0n = rlo + (int64_t)trn * TI, c0n = (int64_t)tcn * TJ;
             j2_issue(src, N, r0n, (int)min((int64_t)TI, rhi - r0n), c0n, TJ, bufs + (b ^ 1) * BW, pitch,
                      &bar[b ^ 1]);
         }
-        mbar_wait(&bar[b], (k >> 1) & 1);
-        const int64_t r0 = rlo + (int64_t)tr * TI, c0 = (tc0 + tc) * (int64_t)TJ;
+        const int64_t r0 = rlo + (int64_t)tr * TI, c0 = (int64_t)tc * TJ;
         const int nr = (int)min((int64_t)TI, rhi - r0);
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
-        const int s0 = (int)((a0 & 15) >> 2), ds = (int)(N & 3);
+        int *buf = bufs + b * BW;
+        int s0 = 0, ds = 0;
+        if (tc >= ca && tc < cb) {
+            mbar_wait(&bar[b], fills[b] & 1);
+            fills[b]++;
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
+            s0 = (int)((a0 & 15) >> 2);
+            ds = (int)(N & 3);
+        } else {
+            for (int e = threadIdx.x; e < (nr + 2) * pitch; e += blockDim.x) {
+                const int rr = e / pitch, cc = e - rr * pitch;
+                const int64_t col = c0 - 4 + cc;
+                buf[e] = (cc < TJ + 8 && col >= 0 && col < N) ? src[(r0 - 1 + rr) * N + col] : 0;
+            }
+            __syncthreads();
+        }
         if (role.passes == 1)
-            j2_march<WIDE>(role, bufs + b * BW, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, vec);
+            j2_march<WIDE>(role, buf, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, true);
         else
-            j2_compute<WIDE>(bufs + b * BW, pitch, s0, ds, dst, N, r0, nr, c0, J, TI, TJ, vec);
+            j2_compute<WIDE>(buf, pitch, s0, ds, dst, N, r0, nr, c0, J, TI, TJ, true);
         tr = trn;
         tc = tcn;
         __syncthreads();
@@ -425,8 +454,8 @@ __device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__
 
 __global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ src, int *__restrict__ dst,
                                                       int64_t N, int64_t rlo, int64_t rhi, int64_t J, int TI,
-                                                      int TJ, int64_t tc0, int64_t ntc, int64_t ntiles,
-                                                      const int *flag, int mode) {
+                                                      int TJ, int64_t ntc, int64_t ca, int64_t cb,
+                                                      int64_t ntiles, const int *flag, int mode) {
     extern __shared__ __align__(128) int smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     int *bufs = smem + 8;
@@ -439,14 +468,15 @@ __global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ sr
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        const int64_t r0 = rlo + (t / ntc) * TI, c0 = (tc0 + t % ntc) * TJ;
+    const int64_t tc = t % ntc;
+    if (threadIdx.x < 32 && tc >= ca && tc < cb) {
+        const int64_t r0 = rlo + (t / ntc) * TI, c0 = tc * TJ;
         j2_issue(src, N, r0, (int)min((int64_t)TI, rhi - r0), c0, TJ, bufs, pitch, &bar[0]);
     }
     if (narrow_mode(mode, flag))
-        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, tc0, ntc, t, ntiles, bar, bufs, true);
+        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, ntiles, bar, bufs);
     else
-        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, tc0, ntc, t, ntiles, bar, bufs, true);
+        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, ntiles, bar, bufs);
 }
 
 template <bool WIDE>
@@ -623,7 +653,6 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
             return after_launch("jacobi1d");
         };
         if (tb > ta) {
-            if ((rc = generic(0, ta)) || (rc = generic(tb, blocks))) return rc;
             const size_t tsmem = 32 + 2 * ((size_t)tile + kTmaPad) * sizeof(int);
             rc = allow_smem((const void *)k_jacobi1d_tma, tsmem);
             if (rc) return rc;
@@ -633,8 +662,9 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi1d_tma, tnt, tsmem);
             int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-            if (grid > tb - ta) grid = tb - ta;
-            k_jacobi1d_tma<<<(unsigned)grid, tnt, tsmem, st>>>(src, dst, lo, hi, x0, tile, ta, tb, flag, mode);
+            if (grid > blocks) grid = blocks;
+            k_jacobi1d_tma<<<(unsigned)grid, tnt, tsmem, st>>>(src, dst, lo, hi, x0, tile, blocks, ta, tb, L.N,
+                                                               flag, mode);
             return after_launch("jacobi1d_tma");
         }
         return generic(0, blocks);
@@ -678,7 +708,6 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
         if (vec && nthreads % 32 == 0 && nthreads <= 512 && room >= 0) cb = room / TJ + 1;
         if (cb > ntj) cb = ntj;
         if (cb - ca >= 1) {
-            if ((rc = generic(0, ca)) || (rc = generic(cb, ntj - cb))) return rc;
             const size_t tsmem = 32 + 2 * (size_t)(TI + 2) * (size_t)(TJ + kRowPad) * sizeof(int);
             rc = allow_smem((const void *)k_jacobi2d_tma, tsmem);
             if (rc) return rc;
@@ -686,11 +715,11 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi2d_tma, (int)nthreads, tsmem);
-            const int64_t ntiles = nti * (cb - ca);
+            const int64_t ntiles = nti * ntj;
             int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
             if (grid > ntiles) grid = ntiles;
             k_jacobi2d_tma<<<(unsigned)grid, (unsigned)nthreads, tsmem, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ,
-                                                                             ca, cb - ca, ntiles, flag, mode);
+                                                                             ntj, ca, cb, ntiles, flag, mode);
             return after_launch("jacobi2d_tma");
         }
         return generic(0, ntj);
