@@ -732,7 +732,7 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
 
 // Device flag: non-zero when the whole double buffer is within the narrow bound.
 int range_flag(const int *a, int64_t n, int bound, int **flag, cudaStream_t st) {
-    cudaError_t err = cudaMallocAsync((void **)flag, sizeof(int), st);
+    cudaError_t err = scratch_alloc((void **)flag, sizeof(int), st);
     if (err != cudaSuccess) return fail(PK_E_ALLOC, "cudaMallocAsync(flag): %s", cudaGetErrorString(err));
     // the flag starts non-zero (bytes 0x01); the check clears it with atomicAnd
     err = cudaMemsetAsync(*flag, 1, sizeof(int), st);

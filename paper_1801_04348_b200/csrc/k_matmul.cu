@@ -21,6 +21,8 @@
 //    a double-buffered shared ring (a transposed on the way in), so each
 //    pair of 128-bit shared loads feeds 64 FFMAs.  Used for the staged leaf
 //    whenever the tile is one of the instantiated shapes.
+#include <type_traits>
+
 #include "pk_internal.cuh"
 
 namespace pk {
@@ -246,6 +248,10 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     T *c = static_cast<T *>(p[2]);
     const int64_t BM = L.B0, BN = L.ub1 * elems(L);
     const bool generic = (L.flags & PK_FLAG_GENERIC) != 0;
+    if constexpr (std::is_same<T, float>::value) {
+        if (L.flags & PK_FLAG_TF32X3)  // optional tensor-core variant, reported separately
+            return launch_matmul_tf32x3(a, b, c, L.N, rlo, rhi, Nc, K, st);
+    }
     if (L.variant == PK_VARIANT_STAGED && !generic && L.N % 4 == 0 && K % 16 == 0 &&
         aligned16(a) && aligned16(b) && aligned16(c) && (rhi - rlo) % BM == 0 && Nc % BN == 0 &&
         rlo % 4 == 0) {

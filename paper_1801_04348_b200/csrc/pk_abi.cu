@@ -39,6 +39,22 @@ int allow_smem(const void *kernel, size_t bytes) {
     return PK_OK;
 }
 
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64) {
+        std::call_once(once[dev], [dev]() {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+        });
+    }
+    return cudaMallocAsync(p, bytes ? bytes : 4, st);
+}
+
 int64_t footprint_words(const pk_launch_t &L) {
     if (L.variant != PK_VARIANT_STAGED) return 0;
     const int64_t E = elems(L);
@@ -101,8 +117,8 @@ int validate(const pk_launch_t *L, int nptrs) {
                        L->family == PK_FAMILY_TRANSPOSE || L->family == PK_FAMILY_REVERSE;
     if (L->dtype != PK_DTYPE_I32 && !(L->dtype == PK_DTYPE_F32 && fp_ok))
         return fail(PK_E_UNSUPPORTED, "dtype %d not provided for family %d", L->dtype, L->family);
-    if (L->flags & PK_FLAG_TF32X3)
-        return fail(PK_E_UNSUPPORTED, "3xTF32 tcgen05 matmul is not built into this library");
+    if ((L->flags & PK_FLAG_TF32X3) && !(L->family == PK_FAMILY_MATMUL && L->dtype == PK_DTYPE_F32))
+        return fail(PK_E_UNSUPPORTED, "3xTF32 applies to float32 matmul only");
     if (L->flags & PK_FLAG_TEMPORAL)
         return fail(PK_E_UNSUPPORTED, "temporally blocked Jacobi is not built into this library");
     return PK_OK;
@@ -193,7 +209,7 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     rc = PK_OK;
     for (int i = 0; i < spec.count && rc == PK_OK; i++) {
         const size_t bytes = (size_t)spec.elems[i] * 4;
-        e = cudaMallocAsync(&dev[i], bytes ? bytes : 4, st);
+        e = scratch_alloc(&dev[i], bytes, st);
         if (e != cudaSuccess) {
             rc = fail(PK_E_ALLOC, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
             break;

@@ -25,6 +25,11 @@ inline int after_launch(const char *what) {
 // Opt a kernel into more than 48 KB of dynamic shared memory.
 int allow_smem(const void *kernel, size_t bytes);
 
+// Stream-ordered scratch allocation from the current device's default pool,
+// which is told (once per device) to keep freed memory: workspaces are
+// re-used across calls instead of being unmapped at every synchronisation.
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
+
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -104,6 +109,8 @@ int sweep_jacobi2d(const pk_launch_t &L, const void *src, void *dst, int64_t lo,
 int jacobi_narrow(const pk_launch_t &L, const void *a, int *narrow, cudaStream_t st);
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
+int launch_matmul_tf32x3(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi,
+                         int64_t Nc, int64_t K, cudaStream_t st);
 int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);
 
 // Shared-memory words staged per block (0 for direct variants).

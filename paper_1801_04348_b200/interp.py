@@ -168,6 +168,7 @@ def run_program(
     inplace: bool = False,
     generic: bool = False,
     case: int | None = None,
+    tf32x3: bool = False,
 ) -> dict:
     """Execute the whole program on the GPU; returns the final array contents.
 
@@ -227,7 +228,8 @@ def run_program(
     kinds = [_kind_of(v) for v in arrays.values()]
     default_kind = kinds[0] if kinds else "list"
 
-    L = binding.make_launch(kind, P, applied, dtype, generic=generic)
+    L = binding.make_launch(kind, P, applied, dtype, generic=generic,
+                            extra_flags=_lib.FLAG_TF32X3 if tf32x3 else 0)
     stream = torch.cuda.current_stream(dev).cuda_stream
 
     with torch.cuda.device(dev):

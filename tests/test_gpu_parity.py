@@ -215,3 +215,21 @@ def test_inputs_not_mutated_and_missing_arrays_zero(cuda):
     assert out["c"] == keep[::-1]
     out = _run(programs.source("reverse"), {"N": 16, "s": 1, "B": 4}, None)
     assert out["a"] == [0] * 16 and out["c"] == [0] * 16
+
+
+def test_matmul_tf32x3_tcgen05_within_tolerance(cuda, oracle_mod):
+    """Optional 3xTF32 tensor-core variant (reported separately): fp32-level
+    accuracy against the binary64 oracle, same tolerance as the FFMA path."""
+    from paper_1801_04348_b200 import programs
+
+    for n in (256, 1024):
+        rng = np.random.default_rng(n + 3)
+        a = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+        b = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+        c = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+        params = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+        got = _run(programs.source("matmul"), params, {"a": a, "b": b, "c": c}, tf32x3=True)["c"]
+        want = oracle_mod.run("matmul", params, {"a": a, "b": b, "c": c})["c"]
+        scale = (np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64))).max()
+        err = np.abs(got.astype(np.float64) - want).max() / scale
+        assert err <= _matmul_tol(n), (n, err)
