@@ -292,9 +292,36 @@ def main() -> int:
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_gf = flop_step / float(e2e_s.item()) / 1e9
-    e2e = {"value": round(e2e_gf, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": 3 * n * n * 4 * world,
-           "d2h_bytes_per_step": n * n * 4 * world,
-           "path": "pk_run_host (C ABI) with pinned host buffers; pk_run_host copies the full arrays"}
+    # per rank: its rows of a and c in, all of b in, its rows of c out (pk_run_host copies the share)
+    e2e = {"value": round(e2e_gf, 1), "unit": "GFLOP/s",
+           "h2d_bytes_per_step": (2 * rows * n + n * n) * 4 * world,
+           "d2h_bytes_per_step": rows * n * 4 * world,
+           "path": "pk_run_host (C ABI) with pinned host buffers, rank share of a/c and all of b"}
+
+    # optional 3xTF32 tcgen05 variant on the same shard (reported separately, never the headline)
+    variants = {}
+    try:
+        Lt = binding.make_launch(kind, tuned, sel.applied, _lib.DTYPE_F32, lo=r0, hi=r0 + rows,
+                                 extra_flags=_lib.FLAG_TF32X3)
+        _lib.launch(Lt, ptrs, st)
+        torch.cuda.synchronize()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(stream)
+        for _ in range(args.steps):
+            _lib.launch(Lt, ptrs, st)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        ms_t = torch.tensor([t0e.elapsed_time(t1e) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        tf = flop_step / (float(ms_t.item()) * 1e-3) / 1e12
+        variants["matmul_tf32x3_tcgen05"] = {
+            "value": round(tf * 1e3, 1), "unit": "GFLOP/s (useful 2n^3)", "ms_per_step": round(float(ms_t.item()), 4),
+            "tensor_tflops": round(3 * tf, 1), "frac_of_tf32_dense": round(3 * tf / (sm_count * 4096 * peaks["sm_max_mhz"] * 1e-6), 4),
+            "note": "3xTF32 split (hi*hi + hi*lo + lo*hi) on tcgen05 kind::tf32, fp32 TMEM accumulation; "
+                    "within the FP32 tolerance, not the FFMA path's rounding sequence"}
+    except (NotImplementedError, ValueError, RuntimeError) as exc:  # shapes the variant does not tile
+        variants["matmul_tf32x3_tcgen05"] = {"unavailable": str(exc)[:200]}
 
     kernels = {}
     cpu = None
@@ -329,6 +356,7 @@ def main() -> int:
             "e2e": e2e,
             "gpu_launches": int(launches),
             "kernels": kernels,
+            "variants": variants,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
@@ -393,8 +421,8 @@ TUNE_GRIDS = {
     "transpose": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((64, 8, 8), (32, 8, 4), (64, 16, 4),
                                                                  (32, 32, 1), (128, 8, 4))],
     "jacobi": [{"B": b, "s": s} for b, s in ((256, 16), (256, 8), (128, 32), (512, 8), (1024, 4))],
-    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((64, 4, 32), (32, 8, 16), (32, 16, 16),
-                                                                (16, 16, 8), (4, 64, 16))],
+    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((32, 8, 32), (64, 4, 32), (32, 8, 16),
+                                                                (8, 32, 16), (16, 16, 32))],
     "matvec": [{"B": b, "s": s} for b, s in ((256, 1), (128, 1), (64, 2), (512, 1), (32, 4))],
 }
 

@@ -123,9 +123,13 @@ int pk_query_machine(int device, pk_machine_t *out);
  * returns after enqueueing.  Replaces interp.run_program (interp.py:215). */
 int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stream);
 
-/* End-to-end call with HOST buffers: pins the host memory, copies in,
- * runs pk_launch, copies the written arrays back and synchronises.  The
- * host buffers are updated in place (inputs and outputs alike). */
+/* End-to-end call with HOST buffers (pass pinned memory for full PCIe
+ * speed): copies the inputs in, runs pk_launch, copies the written arrays
+ * back into the host buffers and synchronises.  With a unit sub-range
+ * (L->hi > 0) only the rank's share crosses PCIe: the rows of row-sharded
+ * operands (matmul a/c, mat-vec a/y, transpose c, addition), the mirrored
+ * range for reversal; replicated operands (b, x, transpose's a) and the
+ * stencil buffers are copied whole. */
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device);
 
 /* One Jacobi sweep over an explicit position range, used by the slab

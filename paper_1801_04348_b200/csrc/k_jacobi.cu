@@ -405,6 +405,11 @@ __device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__
     const int pitch = TJ + kRowPad;
     const int BW = (TI + 2) * pitch;
     const J2Role role = j2_role(TI, TJ, 0);  // fixed for every tile of this block
+    // Tiles in row-major order (column tile fastest), blocks striding by the
+    // grid: at any moment the whole GPU streams a few full row bands, which
+    // keeps DRAM pages and the halo rows shared with the next band hot.
+    // (Giving each block a contiguous run down a column strip instead
+    // scattered the concurrent streams and measured 3x slower.)
     const uint32_t ntc32 = (uint32_t)ntc;
     uint32_t tr = (uint32_t)t / ntc32, tc = (uint32_t)t - tr * ntc32;  // tile -> (row tile, column tile)
     const uint32_t str = (uint32_t)gridDim.x / ntc32, stc = (uint32_t)gridDim.x - str * ntc32;
@@ -459,8 +464,8 @@ __global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ sr
     extern __shared__ __align__(128) int smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     int *bufs = smem + 8;
-    const int64_t t = blockIdx.x;
-    if (t >= ntiles) return;
+    const int64_t t = blockIdx.x, t_end = ntiles;
+    if (t >= t_end) return;
     const int pitch = TJ + kRowPad;
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -474,9 +479,9 @@ __global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ sr
         j2_issue(src, N, r0, (int)min((int64_t)TI, rhi - r0), c0, TJ, bufs, pitch, &bar[0]);
     }
     if (narrow_mode(mode, flag))
-        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, ntiles, bar, bufs);
+        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, t_end, bar, bufs);
     else
-        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, ntiles, bar, bufs);
+        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, t_end, bar, bufs);
 }
 
 template <bool WIDE>

@@ -91,6 +91,41 @@ int array_spec(const pk_launch_t &L, ArraySpec *s) {
     }
 }
 
+// Element range of array i a partitioned launch (lo/hi) reads or writes, so
+// pk_run_host moves only a rank's share across PCIe: rows of the row-sharded
+// operands, the mirrored range for reversal, everything for the stencils.
+void array_range(const pk_launch_t &L, int i, int64_t elems, int64_t *off, int64_t *cnt) {
+    *off = 0;
+    *cnt = elems;
+    if (L.hi <= 0) return;
+    const int64_t N = L.N > 0 ? L.N : 0, lo = L.lo > 0 ? L.lo : 0, hi = L.hi;
+    int64_t a = 0, b = elems;
+    switch (L.family) {
+        case PK_FAMILY_REVERSE:
+            if (i == 0) { a = lo; b = hi; } else { a = N - hi; b = N - lo; }
+            break;
+        case PK_FAMILY_TRANSPOSE:
+            if (i == 1) { a = lo * N; b = hi * N; }
+            break;
+        case PK_FAMILY_MATVEC:
+            if (i == 0) { a = lo * N; b = hi * N; } else if (i == 2) { a = lo; b = hi; }
+            break;
+        case PK_FAMILY_MATMUL:
+            if (i != 1) { a = lo * N; b = hi * N; }
+            break;
+        case PK_FAMILY_ADDITION:
+            a = lo * N;
+            b = hi * N;
+            break;
+        default:
+            break;
+    }
+    if (a < 0) a = 0;
+    if (b > elems) b = elems;
+    *off = a;
+    *cnt = b > a ? b - a : 0;
+}
+
 int dispatch(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     switch (L.family) {
         case PK_FAMILY_REVERSE: return launch_reverse(L, p, st);
@@ -214,18 +249,24 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
             rc = fail(PK_E_ALLOC, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
             break;
         }
-        if (bytes && host_ptrs[i]) {
-            e = cudaMemcpyAsync(dev[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, st);
+        int64_t off, cnt;
+        array_range(*L, i, spec.elems[i], &off, &cnt);
+        char *d = static_cast<char *>(dev[i]) + off * 4;
+        if (cnt && host_ptrs[i]) {
+            e = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * 4, (size_t)cnt * 4,
+                                cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) rc = fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(e));
-        } else if (bytes) {
-            cudaMemsetAsync(dev[i], 0, bytes, st);  // missing arrays are zero-filled (interp.py:79-81)
+        } else if (cnt) {
+            cudaMemsetAsync(d, 0, (size_t)cnt * 4, st);  // missing arrays are zero-filled (interp.py:79-81)
         }
     }
     if (rc == PK_OK) rc = dispatch(*L, dev, st);
     for (int i = 0; i < spec.count && rc == PK_OK; i++) {
-        const size_t bytes = (size_t)spec.elems[i] * 4;
-        if (spec.written[i] && bytes && host_ptrs[i]) {
-            e = cudaMemcpyAsync(host_ptrs[i], dev[i], bytes, cudaMemcpyDeviceToHost, st);
+        int64_t off, cnt;
+        array_range(*L, i, spec.elems[i], &off, &cnt);
+        if (spec.written[i] && cnt && host_ptrs[i]) {
+            e = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * 4, static_cast<char *>(dev[i]) + off * 4,
+                                (size_t)cnt * 4, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) rc = fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(e));
         }
     }

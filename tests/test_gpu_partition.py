@@ -103,3 +103,30 @@ def test_wide_path_for_large_values(cuda, oracle_mod):
     got = run_program(programs.source("jacobi2d"), p2, {"a": a2})["a"]
     want = oracle_mod.run("jacobi2d", p2, {"a": a2})["a"]
     assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+
+
+@pytest.mark.parametrize("family,params", [
+    ("reverse", {"N": 1 << 12, "s": 4, "B": 64}),
+    ("matmul", {"n": 256, "B0": 64, "ub1": 8, "s": 16}),
+    ("matvec", {"N": 256, "s": 1, "B": 64}),
+    ("transpose", {"N": 128, "s": 4, "B0": 32, "B1": 8}),
+    ("addition", {"N": 64, "B0": 4, "B1": 16}),
+])
+def test_run_host_shares_reassemble_oracle(cuda, oracle_mod, family, params):
+    """pk_run_host with a rank's unit range copies only that share; the
+    shares of 3 ranks written into one host buffer equal the oracle."""
+    from paper_1801_04348_b200 import _lib, binding, cases, partition, programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    rng = np.random.default_rng(9)
+    init = {k: rng.integers(-32, 32, size=s).astype(np.int32) for k, s in shapes.items()}
+    want = oracle_mod.run(family, params, init)
+    host = {k: np.ascontiguousarray(v.copy()) for k, v in init.items()}
+    sel = cases.select(kind, params, "nominal")
+    for r in range(3):
+        lo, hi = partition.split(family, params, r, 3)
+        L = binding.make_launch(kind, params, sel.applied, lo=lo, hi=hi)
+        _lib.run_host(L, [host[a.name].ctypes.data for a in programs.FAMILIES[family].arrays], 0)
+    for name in programs.FAMILIES[family].written:
+        assert np.array_equal(host[name].reshape(-1), np.asarray(want[name]).reshape(-1)), name

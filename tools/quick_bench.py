@@ -24,8 +24,8 @@ CONFIGS = {
     "jacobi": [({"T": 10, "N": (1 << 28) + 2, "s": s, "B": b}, 10 * 8 * (1 << 28))
                for (b, s) in [(256, 16), (1024, 4), (256, 8), (256, 32), (128, 32), (512, 8), (128, 16)]],
     "jacobi2d": [({"T": 10, "N": 16386, "s": s, "B0": b0, "B1": b1}, 10 * 8 * 16384**2)
-                 for (b0, b1, s) in [(8, 32, 4), (32, 8, 16), (16, 16, 8), (64, 4, 32), (32, 32, 4),
-                                     (16, 32, 8), (8, 64, 8), (4, 64, 16), (32, 16, 16)]],
+                 for (b0, b1, s) in [(32, 8, 16), (64, 4, 32), (16, 16, 32), (8, 32, 16), (16, 32, 16),
+                                     (8, 64, 16), (32, 8, 32), (16, 8, 64), (8, 16, 64)]],
     "matvec": [({"N": 32768, "s": 1, "B": 256}, 4 * 32768**2),
                ({"N": 32768, "s": 4, "B": 1024}, 4 * 32768**2)],
     "matmul": [({"n": 8192, "B0": 128, "ub1": 8, "s": 16}, 2 * 8192**3),
