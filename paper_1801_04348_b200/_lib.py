@@ -12,7 +12,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libpk.so")
+# PK_LIB_PATH selects an alternative build of the same ABI (kernel-variant experiments)
+LIB_PATH = os.environ.get("PK_LIB_PATH") or os.path.join(PKG, "libpk.so")
 
 # status codes (pk.h)
 PK_OK = 0

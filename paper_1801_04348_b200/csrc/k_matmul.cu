@@ -251,6 +251,10 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     if constexpr (std::is_same<T, float>::value) {
         if (L.flags & PK_FLAG_TF32X3)  // optional tensor-core variant, reported separately
             return launch_matmul_tf32x3(a, b, c, L.N, rlo, rhi, Nc, K, st);
+        // 128 x 128 staged tile fed by TMA (same FFMA chain as the other kernels)
+        if (L.variant == PK_VARIANT_STAGED && !generic && aligned16(a) && aligned16(b) && aligned16(c) &&
+            matmul_tma_fits(L.B0, L.ub1 * elems(L), rhi - rlo, Nc, K, L.N) && rlo % 4 == 0)
+            return launch_matmul_tma(a, b, c, L.N, rlo, rhi, Nc, K, st);
     }
     if (L.variant == PK_VARIANT_STAGED && !generic && L.N % 4 == 0 && K % 16 == 0 &&
         aligned16(a) && aligned16(b) && aligned16(c) && (rhi - rlo) % BM == 0 && Nc % BN == 0 &&

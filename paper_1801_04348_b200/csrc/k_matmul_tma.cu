@@ -1,0 +1,229 @@
+// k_matmul_tma.cu -- the staged matmul leaf with its shared
+// tiles fed by TMA: FP32 on the FFMA pipe, numerics identical to
+// k_matmul_tiled / k_matmul_generic (every output starts from c and runs
+// fma(a[p][k], b[k][q], acc) for k ascending).
+//
+// * a's rows of this launch are transposed once (k_transpose_rows, ~1 % of
+//   the multiply at n = 8192) so both operands are plain 2-D boxes: the
+//   a^T slab BK x BM and the b slab BK x BN of k-step kt are one TMA each.
+// * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage; a
+//   dedicated producer warp issues the TMAs; the 8 compute warps wait on
+//   "full", run BK x 64 FFMAs per thread from 128-bit shared loads, and
+//   release the stage with one arrive per warp on "empty" -- no block-wide
+//   barrier in the main loop, no register staging or shared stores.
+#include <cuda.h>
+
+#include "pk_internal.cuh"
+
+namespace pk {
+namespace {
+
+constexpr int TY = 16, TX = 16;             // compute threads: 16 x 16, 8 x 8 outputs each
+constexpr int BM = 8 * TY, BN = 8 * TX;     // 128 x 128 block tile
+#ifndef PK_MM_BK
+#define PK_MM_BK 16
+#endif
+#ifndef PK_MM_STAGES
+#define PK_MM_STAGES 4
+#endif
+constexpr int BK = PK_MM_BK;                // k slab per stage
+constexpr int STAGES = PK_MM_STAGES;
+constexpr int NCOMP = TY * TX;              // 256 compute threads
+constexpr int NTHREADS = NCOMP;             // thread 0 also issues the TMAs
+constexpr int A_SLAB = BK * BM * 4, B_SLAB = BK * BN * 4;
+constexpr int STAGE_BYTES = A_SLAB + B_SLAB;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;
+
+// out[k][r] = a[r][k] for r < rows (row-major a with leading dimension lda)
+__global__ void __launch_bounds__(256) k_transpose_rows(const float *__restrict__ a, float *__restrict__ out,
+                                                       int64_t rows, int64_t K, int64_t lda) {
+    __shared__ float t[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) t[r][tx] = a[(r0 + r) * lda + k0 + tx];
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) out[(k0 + r) * rows + r0 + tx] = t[tx][r];
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+#ifndef PK_MM_FMA2
+#define PK_MM_FMA2 1  // measured 57.8 vs 55.7 TFLOP/s at n = 8192 (half the FP32 issue slots)
+#endif
+
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+// (c0, c1) = (a.lo * b.lo + c0, a.hi * b.hi + c1), each an IEEE fma.rn
+__device__ __forceinline__ void fma2(float &c0, float &c1, unsigned long long a, unsigned long long b) {
+    unsigned long long c = pack2(c0, c1);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+    c0 = __uint_as_float((unsigned)(c & 0xffffffffu));
+    c1 = __uint_as_float((unsigned)(c >> 32));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
+                                                          const __grid_constant__ CUtensorMap map_b,
+                                                          float *__restrict__ C, int64_t ldc, int64_t rlo,
+                                                          int ntn, int ktiles) {
+    extern __shared__ unsigned char smem_raw[];
+    // align by offsetting the shared array itself (not via an integer cast), so
+    // the compiler keeps the shared address space and emits LDS, not generic LD
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    uint64_t *empty = full + STAGES;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tm = blockIdx.x / ntn, tn = blockIdx.x % ntn;
+    const int m0 = tm * BM, n0 = tn * BN;  // m0 relative to this launch's first row
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCOMP / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // thread 0 doubles as the TMA producer: stage kt is refilled with slab
+    // kt + STAGES - 1 as soon as every warp has released it
+    auto produce = [&](int kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+        unsigned char *st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(st, &map_at, &full[s], m0, kt * BK);
+        tma_load_2d(st + A_SLAB, &map_b, &full[s], n0, kt * BK);
+    };
+    if (tid == 0)
+        for (int kt = 0; kt < STAGES - 1 && kt < ktiles; kt++) produce(kt);
+    (void)warp;
+
+    // ---- compute (all 8 warps)
+    const int tx = tid % TX, ty = tid / TX;
+    float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
+    const int64_t chalf = (int64_t)(BM / 2) * ldc;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
+        const float4 l = *reinterpret_cast<const float4 *>(cr);
+        const float4 h = *reinterpret_cast<const float4 *>(cr + BN / 2);
+        acc[i][0] = l.x; acc[i][1] = l.y; acc[i][2] = l.z; acc[i][3] = l.w;
+        acc[i][4] = h.x; acc[i][5] = h.y; acc[i][6] = h.z; acc[i][7] = h.w;
+    }
+    for (int kt = 0; kt < ktiles; kt++) {
+        const int s = kt % STAGES;
+        if (tid == 0 && kt + STAGES - 1 < ktiles) produce(kt + STAGES - 1);
+        mbar_wait(&full[s], (kt / STAGES) & 1);
+        const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM]
+        const float *Bs = As + BK * BM;                                               // [BK][BN]
+#pragma unroll
+        for (int kk = 0; kk < BK; kk++) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
+            const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
+            const float4 b0 = *reinterpret_cast<const float4 *>(Bs + kk * BN + tx * 4);
+            const float4 b1 = *reinterpret_cast<const float4 *>(Bs + kk * BN + BN / 2 + tx * 4);
+            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#if PK_MM_FMA2
+            // sm_100 packed fp32 FMA: two IEEE fma.rn per instruction (same bits as FFMA)
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const unsigned long long ai = pack2(af[i], af[i]);
+#pragma unroll
+                for (int j = 0; j < 8; j += 2) fma2(acc[i][j], acc[i][j + 1], ai, pack2(bf[j], bf[j + 1]));
+            }
+#else
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 8; j++) acc[i][j] = __fmaf_rn(af[i], bf[j], acc[i][j]);
+#endif
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
+        *reinterpret_cast<float4 *>(cr) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        *reinterpret_cast<float4 *>(cr + BN / 2) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+// rows x cols fp32 row-major, box box_rows x box_cols, no swizzle (plain row-major slab in smem)
+int make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+             int box_rows) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) return fail(PK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PK_OK;
+}
+
+}  // namespace
+
+// True when the TMA-fed kernel tiles this launch (128 x 128 block tile).
+bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n) {
+    return BM_case == BM && BN_case == BN && rows % BM == 0 && Nc % BN == 0 && K % BK == 0 && K > 0 &&
+           n % 4 == 0 && n <= ((int64_t)1 << 30);
+}
+
+int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
+                      int64_t K, cudaStream_t st) {
+    const int64_t rows = rhi - rlo;
+    float *at = nullptr;
+    cudaError_t e = scratch_alloc((void **)&at, (size_t)rows * K * sizeof(float), st);
+    if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul a^T workspace: %s", cudaGetErrorString(e));
+    int rc = PK_OK;
+    k_transpose_rows<<<dim3((unsigned)(K / 32), (unsigned)(rows / 32)), 256, 0, st>>>(a + rlo * n, at, rows, K, n);
+    if ((rc = after_launch("matmul_transpose_a")) == PK_OK) {
+        CUtensorMap mat, mb;
+        if ((rc = make_map(&mat, at, K, rows, rows, BM, BK)) == PK_OK &&
+            (rc = make_map(&mb, b, K, Nc, n, BN, BK)) == PK_OK &&
+            (rc = allow_smem((const void *)k_matmul_tma, SMEM_BYTES)) == PK_OK) {
+            const int ntn = (int)(Nc / BN);
+            k_matmul_tma<<<(unsigned)((rows / BM) * ntn), NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn,
+                                                                                       (int)(K / BK));
+            rc = after_launch("matmul_tma");
+        }
+    }
+    cudaFreeAsync(at, st);
+    return rc;
+}
+
+}  // namespace pk

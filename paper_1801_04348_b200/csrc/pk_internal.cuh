@@ -109,6 +109,9 @@ int sweep_jacobi2d(const pk_launch_t &L, const void *src, void *dst, int64_t lo,
 int jacobi_narrow(const pk_launch_t &L, const void *a, int *narrow, cudaStream_t st);
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
+bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n);
+int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
+                      int64_t K, cudaStream_t st);
 int launch_matmul_tf32x3(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi,
                          int64_t Nc, int64_t K, cudaStream_t st);
 int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);

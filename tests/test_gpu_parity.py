@@ -185,10 +185,11 @@ def test_tuned_and_generic_matmul_bit_identical(cuda):
     n = 256
     rng = np.random.default_rng(5)
     arrays = {k: rng.standard_normal((n, n)).astype(np.float32) for k in "abc"}
-    params = {"n": n, "B0": 64, "ub1": 8, "s": 8}
-    t = _run(programs.source("matmul"), params, arrays)["c"]
-    g = _run(programs.source("matmul"), params, arrays, generic=True)["c"]
-    assert np.array_equal(t.view(np.uint32), g.view(np.uint32))
+    # 64 x 64 register-blocked tile; 128 x 128 TMA-fed tile (packed f32x2 FMAs)
+    for params in ({"n": n, "B0": 64, "ub1": 8, "s": 8}, {"n": n, "B0": 128, "ub1": 8, "s": 16}):
+        t = _run(programs.source("matmul"), params, arrays)["c"]
+        g = _run(programs.source("matmul"), params, arrays, generic=True)["c"]
+        assert np.array_equal(t.view(np.uint32), g.view(np.uint32)), params
 
 
 def test_errors_mirror_reference(cuda):
