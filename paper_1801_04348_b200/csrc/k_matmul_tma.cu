@@ -52,19 +52,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-#ifndef PK_MM_FMA2
-#define PK_MM_FMA2 1  // measured 57.8 vs 55.7 TFLOP/s at n = 8192 (half the FP32 issue slots)
-#endif
-
+// sm_100 packed fp32 FMA (fma.rn.f32x2): two IEEE fma.rn per instruction --
+// the same bits as two FFMAs, half the issue slots (57.8 vs 55.7 TFLOP/s).
 __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
     return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
 }
-// (c0, c1) = (a.lo * b.lo + c0, a.hi * b.hi + c1), each an IEEE fma.rn
-__device__ __forceinline__ void fma2(float &c0, float &c1, unsigned long long a, unsigned long long b) {
-    unsigned long long c = pack2(c0, c1);
+// c = {a.lo * b.lo + c.lo, a.hi * b.hi + c.hi}
+__device__ __forceinline__ void fma2p(unsigned long long &c, unsigned long long a, unsigned long long b) {
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
-    c0 = __uint_as_float((unsigned)(c & 0xffffffffu));
-    c1 = __uint_as_float((unsigned)(c >> 32));
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -82,7 +77,16 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int tm = blockIdx.x / ntn, tn = blockIdx.x % ntn;
+    // grouped raster: blocks launched together cover a GROUP x (all columns)
+    // band walked column-group by column-group, so the a rows and b columns
+    // a wave touches stay resident in L2
+    constexpr int GROUP = 8;
+    const int ntm = (int)(gridDim.x / ntn);
+    const int per_group = GROUP * ntn;
+    const int g = blockIdx.x / per_group, first = g * GROUP;
+    const int gsize = min(ntm - first, GROUP);
+    const int local = blockIdx.x - g * per_group;
+    const int tm = first + local % gsize, tn = local / gsize;
     const int m0 = tm * BM, n0 = tn * BN;  // m0 relative to this launch's first row
 
     if (tid == 0) {
@@ -112,14 +116,15 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
     const int tx = tid % TX, ty = tid / TX;
     float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
     const int64_t chalf = (int64_t)(BM / 2) * ldc;
-    float acc[8][8];
+    // accumulators as packed column pairs: acc[i][jp] = {c[i][2jp], c[i][2jp+1]}
+    // (the operand format of fma.rn.f32x2, so the loop never repacks them)
+    unsigned long long acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; i++) {
         const float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
-        const float4 l = *reinterpret_cast<const float4 *>(cr);
-        const float4 h = *reinterpret_cast<const float4 *>(cr + BN / 2);
-        acc[i][0] = l.x; acc[i][1] = l.y; acc[i][2] = l.z; acc[i][3] = l.w;
-        acc[i][4] = h.x; acc[i][5] = h.y; acc[i][6] = h.z; acc[i][7] = h.w;
+        const ulonglong2 l = *reinterpret_cast<const ulonglong2 *>(cr);
+        const ulonglong2 h = *reinterpret_cast<const ulonglong2 *>(cr + BN / 2);
+        acc[i][0] = l.x; acc[i][1] = l.y; acc[i][2] = h.x; acc[i][3] = h.y;
     }
     for (int kt = 0; kt < ktiles; kt++) {
         const int s = kt % STAGES;
@@ -131,24 +136,16 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
         for (int kk = 0; kk < BK; kk++) {
             const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
             const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
-            const float4 b0 = *reinterpret_cast<const float4 *>(Bs + kk * BN + tx * 4);
-            const float4 b1 = *reinterpret_cast<const float4 *>(Bs + kk * BN + BN / 2 + tx * 4);
+            const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + tx * 4);
+            const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + BN / 2 + tx * 4);
             const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#if PK_MM_FMA2
-            // sm_100 packed fp32 FMA: two IEEE fma.rn per instruction (same bits as FFMA)
+            const unsigned long long bp[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
             for (int i = 0; i < 8; i++) {
                 const unsigned long long ai = pack2(af[i], af[i]);
 #pragma unroll
-                for (int j = 0; j < 8; j += 2) fma2(acc[i][j], acc[i][j + 1], ai, pack2(bf[j], bf[j + 1]));
+                for (int jp = 0; jp < 4; jp++) fma2p(acc[i][jp], ai, bp[jp]);
             }
-#else
-#pragma unroll
-            for (int i = 0; i < 8; i++)
-#pragma unroll
-                for (int j = 0; j < 8; j++) acc[i][j] = __fmaf_rn(af[i], bf[j], acc[i][j]);
-#endif
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
@@ -156,8 +153,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
 #pragma unroll
     for (int i = 0; i < 8; i++) {
         float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
-        *reinterpret_cast<float4 *>(cr) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        *reinterpret_cast<float4 *>(cr + BN / 2) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        *reinterpret_cast<ulonglong2 *>(cr) = make_ulonglong2(acc[i][0], acc[i][1]);
+        *reinterpret_cast<ulonglong2 *>(cr + BN / 2) = make_ulonglong2(acc[i][2], acc[i][3]);
     }
 }
 
