@@ -1,0 +1,56 @@
+"""Randomised parity: many small parameter draws per family (tails, odd
+extents, block sizes that are not warp multiples, every leaf), CUDA vs the
+CPU oracle, bit-exact.  Seeds are fixed so failures reproduce."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _draw(family, rng):
+    r = lambda lo, hi: int(rng.integers(lo, hi))  # noqa: E731
+    if family == "reverse":
+        return {"N": r(1, 5000), "s": r(1, 9), "B": r(1, 300)}
+    if family == "transpose":
+        return {"N": r(1, 300), "s": r(1, 5), "B0": r(1, 70), "B1": r(1, 40)}
+    if family == "jacobi":
+        return {"T": r(0, 7), "N": r(2, 6000), "s": r(1, 9), "B": r(1, 300)}
+    if family == "jacobi2d":
+        return {"T": r(0, 5), "N": r(3, 200), "s": r(1, 9), "B0": r(1, 40), "B1": r(1, 40)}
+    if family == "matvec":
+        return {"N": r(1, 300), "s": r(1, 5), "B": r(1, 300)}
+    if family == "matmul":
+        return {"n": r(1, 200), "B0": r(1, 40), "ub1": r(1, 20), "s": r(1, 9)}
+    return {"N": r(1, 200), "B0": r(1, 40), "B1": r(1, 40)}
+
+
+def _threads_ok(family, P):
+    from paper_1801_04348_b200 import programs
+
+    return programs.threads_per_block(family, P) <= 1024
+
+
+@pytest.mark.parametrize("family", ["reverse", "transpose", "jacobi", "jacobi2d", "matvec", "matmul", "addition"])
+def test_random_parameters_match_oracle(cuda, oracle_mod, family):
+    from paper_1801_04348_b200 import case_table, programs, run_program
+
+    rng = np.random.default_rng(0xF022 + hash(family) % 1000)
+    kind = programs.original(family)
+    ncases = len(case_table(family, "b200").cases)
+    done = 0
+    while done < 25:
+        P = _draw(family, rng)
+        if not _threads_ok(family, P):
+            continue
+        shapes = programs.array_shapes(kind, P)
+        lim = 1 << 6 if family in ("matvec", "matmul") else 1 << 30
+        arrays = {k: rng.integers(-lim, lim, size=s).astype(np.int32) for k, s in shapes.items()}
+        want = oracle_mod.run(family, P, arrays)
+        case = int(rng.integers(1, ncases + 1))
+        generic = bool(rng.integers(0, 2))
+        got = run_program(kind.text, P, arrays, case=case, generic=generic)
+        for name in programs.FAMILIES[family].written:
+            assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), \
+                (family, P, case, generic, name)
+        done += 1
