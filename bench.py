@@ -409,6 +409,24 @@ def bench_kernels(peaks, mv) -> dict:
         out[fam] = {"params": run_params, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
                     "value": round(gbs, 1), "unit": unit, "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
                     "frac_of_8tbs": round(gbs / 8000.0, 4), "tuning_trials": len(trials)}
+        if fam == "jacobi":  # temporally blocked variant, reported separately (same results)
+            for h in (7, 15):
+                Lt = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32,
+                                         extra_flags=_lib.FLAG_TEMPORAL)
+                Lt.tblock = h
+                _lib.launch(Lt, ptrs, st.cuda_stream)
+                torch.cuda.synchronize()
+                e0.record(st)
+                _lib.launch(Lt, ptrs, st.cuda_stream)
+                e1.record(st)
+                torch.cuda.synchronize()
+                tms = e0.elapsed_time(e1)
+                tg = work / (tms * 1e-3) / 1e9
+                out["jacobi_temporal_h%d" % h] = {
+                    "params": run_params, "ms": round(tms, 3), "value": round(tg, 1), "unit": unit,
+                    "speedup_vs_per_step": round(ms / tms, 2),
+                    "note": "algorithmic bytes of the per-step program / time: exceeds the HBM roofline "
+                            "because h steps share one HBM pass; results bit-identical"}
         del bufs
         torch.cuda.empty_cache()
     return out

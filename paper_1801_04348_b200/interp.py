@@ -169,12 +169,16 @@ def run_program(
     generic: bool = False,
     case: int | None = None,
     tf32x3: bool = False,
+    temporal: int = 0,
 ) -> dict:
     """Execute the whole program on the GPU; returns the final array contents.
 
     ``machine``: the machine values for case selection (default: the live
     device).  ``case``: force a leaf by index (tests / tuner).  ``generic``:
     force the program's literal thread mapping instead of the tuned tile.
+    Optional variants, reported separately from the leaves: ``tf32x3``
+    (float32 matmul on tcgen05, fp32-level accuracy) and ``temporal=h``
+    (1-D Jacobi advancing h steps per HBM pass, bit-identical).
     """
     global _last
     if tracer is not None:
@@ -229,7 +233,9 @@ def run_program(
     default_kind = kinds[0] if kinds else "list"
 
     L = binding.make_launch(kind, P, applied, dtype, generic=generic,
-                            extra_flags=_lib.FLAG_TF32X3 if tf32x3 else 0)
+                            extra_flags=(_lib.FLAG_TF32X3 if tf32x3 else 0) | (_lib.FLAG_TEMPORAL if temporal else 0))
+    if temporal:
+        L.tblock = int(temporal)  # steps fused per HBM pass (odd; 1-D Jacobi only)
     stream = torch.cuda.current_stream(dev).cuda_stream
 
     with torch.cuda.device(dev):

@@ -1,0 +1,33 @@
+"""Optional variants reported beside the leaves: temporally blocked 1-D
+Jacobi (bit-identical to the per-step program) and its half bookkeeping."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("h", [3, 7, 9])
+@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 8, 11, 20])
+def test_temporal_jacobi1d_matches_oracle(cuda, oracle_mod, h, T):
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(T * 31 + h)
+    for N, s, B in ((20002, 4, 64), (9001, 3, 100)):  # full coverage; tail + odd N
+        params = {"T": T, "N": N, "s": s, "B": B}
+        a = rng.integers(-(1 << 20), 1 << 20, size=2 * N).astype(np.int32)
+        want = oracle_mod.run("jacobi", params, {"a": a})["a"]
+        got = run_program(programs.source("jacobi"), params, {"a": a}, temporal=h)["a"]
+        assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1)), (T, h, N)
+
+
+def test_temporal_jacobi1d_wide_values(cuda, oracle_mod):
+    """Full-range int32 inputs force 64-bit sums inside the fused steps too."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(4)
+    params = {"T": 13, "N": 40002, "s": 8, "B": 128}
+    a = rng.integers(-(2**31), 2**31 - 1, size=2 * params["N"]).astype(np.int32)
+    want = oracle_mod.run("jacobi", params, {"a": a})["a"]
+    got = run_program(programs.source("jacobi"), params, {"a": a}, temporal=5)["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
