@@ -328,6 +328,10 @@ def main() -> int:
     if rank == 0 and world == 1 and not args.no_kernels:
         del ha, hb, hc
         kernels = bench_kernels(peaks, mv)
+        try:
+            kernels["emitted_baseline"] = bench_emitted(kernels)
+        except Exception as exc:  # the baseline is informative only
+            kernels["emitted_baseline"] = {"unavailable": str(exc)[:200]}
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = cpu_cores()
         gf, runs, sec = cpu_matmul_sample(1024, threads, budget_s=10.0)
@@ -427,6 +431,55 @@ def bench_kernels(peaks, mv) -> dict:
                     "speedup_vs_per_step": round(ms / tms, 2),
                     "note": "algorithmic bytes of the per-step program / time: exceeds the HBM roofline "
                             "because h steps share one HBM pass; results bit-identical"}
+        del bufs
+        torch.cuda.empty_cache()
+    return out
+
+
+EMITTED_CONFIGS = {
+    # program: (params, algorithmic work, unit) -- the reference's emitted leaf text
+    # (static shared memory, grid capped at 256 blocks), compiled with NVRTC
+    "reverse": ({"N": 1 << 30, "s": 16, "B": 256}, 8 * (1 << 30), "GB/s"),
+    "transpose": ({"N": 32768, "s": 4, "B0": 32, "B1": 8}, 8 * 32768 * 32768, "GB/s"),
+    "jacobi": ({"T": 10, "N": (1 << 28) + 2, "s": 16, "B": 256}, 10 * 8 * (1 << 28), "GB/s"),
+    "matvec": ({"N": 8192, "s": 1, "B": 256}, 4 * 8192 * 8192 + 8 * 8192, "GB/s"),
+    "matmul": ({"n": 4096, "B0": 32, "ub1": 8, "s": 4}, 2 * 4096**3, "GFLOP/s"),
+}
+
+
+def bench_emitted(ours: dict) -> dict:
+    """The "naive emitted kernel" bar: the reference's own
+    CUDA text for the original program, compiled for sm_100a at load time."""
+    import torch
+
+    from paper_1801_04348_b200 import jit
+
+    path = os.path.join(REPO, "tests", "golden", "emitted_leaves.json")
+    with open(path) as fh:
+        entries = {(e["program"], e["variant"]): e for e in json.load(fh)["entries"]}
+    out = {}
+    for prog, (params, work, unit) in EMITTED_CONFIGS.items():
+        leaf = jit.Leaf.from_json(entries[(prog, "original")]["leaf"])
+        shapes = jit.array_shapes(leaf, params)
+        bufs = {}
+        for name, shape in shapes.items():
+            n = jit.eval_product(shape)
+            if unit == "GFLOP/s":
+                bufs[name] = torch.randint(-4, 4, (n,), dtype=torch.int32, device="cuda")
+            else:
+                bufs[name] = torch.randint(-(1 << 20), 1 << 20, (n,), dtype=torch.int32, device="cuda")
+        st = torch.cuda.current_stream()
+        jit.run_leaf(leaf, params, bufs, st.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        jit.run_leaf(leaf, params, bufs, st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        val = work / (ms * 1e-3) / 1e9
+        out[prog] = {"params": params, "ms": round(ms, 3), "value": round(val, 1), "unit": unit,
+                     "kernel": leaf.kernel_name}
         del bufs
         torch.cuda.empty_cache()
     return out

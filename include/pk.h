@@ -146,6 +146,16 @@ int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo
  * every later step too).  Synchronises `stream`. */
 int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void *stream);
 
+/* Load-time compilation for programs outside the seven families: CUDA text
+ * (the reference's emitted leaf, pkg/src/parakern/emit.py:268-594) compiled
+ * for sm_100a with NVRTC, then launched with explicit geometry.  kinds[i]:
+ * 0 = int32 scalar, 1 = device pointer; args[i] holds the value. */
+int pk_jit_compile(const char *source, const char *kernel_name, const char *const *options, int nopts,
+                   void **handle);
+int pk_jit_launch(void *handle, const uint32_t *grid, const uint32_t *block, uint32_t smem_bytes,
+                  const uint64_t *args, const int32_t *kinds, int nargs, void *stream);
+int pk_jit_release(void *handle);
+
 /* Shared-memory words the leaf kernel stages per block (the footprint the
  * case constrains against Z_B; reference counters.py:416-464). */
 int64_t pk_footprint_words(const pk_launch_t *L);

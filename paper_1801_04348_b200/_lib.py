@@ -59,6 +59,9 @@ EXPORTS = (
     "pk_launch_count",
     "pk_last_error",
     "pk_version",
+    "pk_jit_compile",
+    "pk_jit_launch",
+    "pk_jit_release",
 )
 
 
@@ -147,6 +150,15 @@ def load() -> ctypes.CDLL:
         lib.pk_launch_count.restype = ctypes.c_int64
         lib.pk_last_error.argtypes = []
         lib.pk_last_error.restype = ctypes.c_char_p
+        lib.pk_jit_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p),
+                                       ctypes.c_int, ctypes.POINTER(vp)]
+        lib.pk_jit_compile.restype = ctypes.c_int
+        lib.pk_jit_launch.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
+                                      ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.POINTER(ctypes.c_int32), ctypes.c_int, vp]
+        lib.pk_jit_launch.restype = ctypes.c_int
+        lib.pk_jit_release.argtypes = [vp]
+        lib.pk_jit_release.restype = ctypes.c_int
         lib.pk_version.argtypes = []
         lib.pk_version.restype = ctypes.c_int
         _lib = lib
@@ -222,6 +234,27 @@ def query_machine(device: int = 0) -> dict:
     out = {name: getattr(m, name) for name, _ in PkMachine._fields_}
     out["name"] = m.name.decode("utf-8", "replace")
     return out
+
+
+def jit_compile(source: str, name: str, options=()) -> int:
+    """Compile CUDA text for sm_100a (NVRTC); returns an opaque kernel handle."""
+    h = ctypes.c_void_p()
+    opts = (ctypes.c_char_p * max(1, len(options)))(*[o.encode() for o in options])
+    check(load().pk_jit_compile(source.encode(), name.encode(), opts, len(options), ctypes.byref(h)))
+    return int(h.value)
+
+
+def jit_launch(handle: int, grid, block, args, kinds, smem: int = 0, stream: int = 0) -> None:
+    g = (ctypes.c_uint32 * 3)(*(list(grid) + [1] * (3 - len(grid))))
+    b = (ctypes.c_uint32 * 3)(*(list(block) + [1] * (3 - len(block))))
+    n = len(args)
+    av = (ctypes.c_uint64 * max(1, n))(*[int(x) & 0xFFFFFFFFFFFFFFFF for x in args])
+    kv = (ctypes.c_int32 * max(1, n))(*kinds)
+    check(load().pk_jit_launch(ctypes.c_void_p(handle), g, b, smem, av, kv, n, ctypes.c_void_p(stream or None)))
+
+
+def jit_release(handle: int) -> None:
+    load().pk_jit_release(ctypes.c_void_p(handle))
 
 
 def version() -> tuple[int, int]:

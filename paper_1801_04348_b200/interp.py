@@ -186,7 +186,18 @@ def run_program(
             "tracer is CPU-only instrumentation of the reference interpreter; "
             "the GPU executor cannot report per-access events"
         )
-    kind = identify(program)
+    try:
+        kind = identify(program)
+    except NotImplementedError:
+        # outside the seven families: compile the reference's own emitted leaf
+        # for sm_100a (NVRTC) when parakern is here to emit it (jit.py)
+        if not (hasattr(program, "decls") and hasattr(program, "top")):
+            raise
+        from . import jit
+
+        leaf = jit.emit_leaf(program, params)
+        _last = RunInfo("emitted", None, tuple(leaf.applied), False, {"kernel": leaf.kernel_name}, 0)
+        return jit.run_program_jit(leaf, params, arrays)
     P = effective_params(kind, params)
     fam = FAMILIES[kind.family]
     torch = _torch()
