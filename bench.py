@@ -336,7 +336,7 @@ def main() -> int:
         threads = cpu_cores()
         gf, runs, sec = cpu_matmul_sample(1024, threads, budget_s=10.0)
         cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-               "sample": "oracle/pk_oracle.c binary64 matmul n=1024 (2.15 GFLOP) x %d runs, %.1f s/run; "
+               "sample": "oracle/pk_oracle.c binary64 matmul n=1024 (2.15 GFLOP) x %d runs, %.3f s/run; "
                          "the reference interpreter itself ran 46k FMA/s on 1 core (SURVEY 6)" % (runs, sec)}
 
     if rank == 0:
