@@ -90,10 +90,10 @@ __device__ __forceinline__ void store4(int *dst, int64_t x, int64_t lo, int64_t 
 
 // Outputs x = xs + 4p .. +3 from a shared window whose index 0 holds
 // position xs - 4 (sb is 16-byte aligned when al16, else 8-byte aligned).
-template <bool WIDE>
+template <bool WIDE, bool FULL = false>  // FULL: every warp of the group has 32 lanes
 __device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__restrict__ dst, int64_t lo,
-                                           int64_t hi, int64_t xs, int tile, bool vec) {
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+                                           int64_t hi, int64_t xs, int tile, bool vec, int tid, int nt) {
+    const int lane = tid & 31;
     const int wlanes = min(32, nt - (tid - lane));  // lanes of this (possibly partial) warp
     const unsigned wmask = wlanes == 32 ? 0xffffffffu : ((1u << wlanes) - 1u);
     const int quads = tile >> 2;
@@ -110,8 +110,8 @@ __device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__rest
                 c = make_int4(u.x, u.y, w.x, w.y);
             }
         }
-        int l = __shfl_up_sync(wmask, c.w, 1);
-        int r = __shfl_down_sync(wmask, c.x, 1);
+        int l = __shfl_up_sync(FULL ? 0xffffffffu : wmask, c.w, 1);
+        int r = __shfl_down_sync(FULL ? 0xffffffffu : wmask, c.x, 1);
         if (!act) continue;
         if (lane == 0) l = sb[4 * p + 3];
         if (lane + 1 == wlanes || p + 1 == quads) r = sb[4 * p + 8];
@@ -122,17 +122,19 @@ __device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__rest
     }
 }
 
-// Persistent TMA pipeline for interior tiles (whole window inside the
-// half): each block walks tiles t_begin + blockIdx.x + k*gridDim.x; one
-// thread issues a cp.async.bulk of tile k+1's window into the other shared
-// buffer while the block computes tile k, completion tracked by one
-// mbarrier per buffer.  The window start is rounded down to 16 bytes (TMA
-// alignment); its 8-byte remainder is the per-tile shift.
-constexpr int kTmaPad = 16;  // words of slack per buffer for the alignment shift
+// Persistent, warp-specialised TMA pipeline.  Each block walks tiles
+// blockIdx.x + k*gridDim.x through an S-stage ring of shared windows: warp 0
+// (the producer) fills window k mod S with one cp.async.bulk (the window
+// start rounded down to 16 bytes; the 8-byte remainder is the tile's shift)
+// as soon as the consumers have released it, and the other warps compute.
+// full[b] completes when window b has landed (TMA transaction count, or the
+// producer's arrive after a guarded fill); empty[b] when every consumer warp
+// has finished reading it.  No block-wide barrier: each consumer warp runs
+// ahead to the next landed window on its own.
+constexpr int kTmaPad = 16;    // words of slack per buffer for the alignment shift
+constexpr int kMaxStages = 8;  // ring depth limit (mbarrier header: 2 x 8 x 8 bytes)
+constexpr int kRingHeader = 2 * kMaxStages * 2;  // header size in ints
 
-// Tiles [ta, tb) have their whole rounded window inside the half and are
-// TMA-fed; the edge tiles outside it (at most one or two per sweep) are
-// filled by guarded loads of the whole block, in turn, from the same loop.
 __device__ __forceinline__ void j1_issue(const int *src, int64_t xs, int tile, int *buf, uint64_t *bar) {
     const uintptr_t ga = reinterpret_cast<uintptr_t>(src + xs - 4);
     const int shift = (int)((ga & 15) >> 2);
@@ -141,58 +143,90 @@ __device__ __forceinline__ void j1_issue(const int *src, int64_t xs, int tile, i
     tma_load_1d(buf, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, bar);
 }
 
-template <bool WIDE>
-__device__ __forceinline__ void j1_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t lo,
-                                            int64_t hi, int64_t x0, int tile, int64_t t, int64_t ntiles,
-                                            int64_t ta, int64_t tb, int64_t limit, uint64_t *bar, int *bufs) {
+// Producer warp.  Tiles [ta, tb) have their whole rounded window inside the
+// half and go by TMA; the one or two edge tiles outside it are filled by
+// guarded loads of the warp itself.
+__device__ __forceinline__ void j1_produce(const int *__restrict__ src, int64_t x0, int tile, int64_t ntiles,
+                                           int64_t ta, int64_t tb, int64_t limit, int S, uint64_t *full,
+                                           uint64_t *empty, int *bufs) {
+    const int lane = threadIdx.x & 31;
     const int BW = tile + kTmaPad;
-    uint32_t fills[2] = {0u, 0u};  // completed TMA phases per buffer (block-uniform)
-    for (int k = 0; t < ntiles; k++, t += gridDim.x) {
-        const int b = k & 1;
-        const int64_t tn = t + gridDim.x;
-        if (threadIdx.x == 0 && tn < ntiles && tn >= ta && tn < tb) {
-            fence_proxy_async();
-            j1_issue(src, x0 + tn * tile, tile, bufs + (b ^ 1) * BW, &bar[b ^ 1]);
-        }
-        const int64_t xs = x0 + t * tile;
+    uint32_t ephase = 0u;  // bit b: parity of empty[b]'s next completion
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // a fresh barrier reports the phase before its first as complete:
+        // the first S waits pass at once
+        mbar_wait(&empty[b], ((ephase >> b) & 1u) ^ 1u);
+        ephase ^= 1u << b;
         int *buf = bufs + b * BW;
-        int shift = 0;
+        const int64_t xs = x0 + t * tile;
         if (t >= ta && t < tb) {
-            mbar_wait(&bar[b], fills[b] & 1);
-            fills[b]++;
-            shift = (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2);
+            if (lane == 0) {
+                fence_proxy_async();  // earlier generic accesses of buf before the async write
+                j1_issue(src, xs, tile, buf, &full[b]);
+            }
         } else {
-            for (int q = threadIdx.x; q < tile + 8; q += blockDim.x) {
+            for (int q = lane; q < tile + 8; q += 32) {
                 const int64_t i = xs - 4 + q;
                 buf[q] = (i >= 0 && i < limit) ? src[i] : 0;
             }
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[b]);
         }
-        j1_compute<WIDE>(buf + shift, shift == 0, dst, lo, hi, xs, tile, true);
-        __syncthreads();  // buffer b is refilled at iteration k+1
+        b = b + 1 == S ? 0 : b + 1;
     }
 }
 
-__global__ void __launch_bounds__(256) k_jacobi1d_tma(const int *__restrict__ src, int *__restrict__ dst,
+template <bool WIDE, bool FULL>
+__device__ __forceinline__ void j1_consume(const int *__restrict__ src, int *__restrict__ dst, int64_t lo,
+                                           int64_t hi, int64_t x0, int tile, int64_t ntiles, int64_t ta,
+                                           int64_t tb, int S, uint64_t *full, uint64_t *empty, int *bufs,
+                                           int ctid, int nct) {
+    const int BW = tile + kTmaPad;
+    uint32_t fphase = 0u;  // bit b: parity of full[b]'s next completion
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&full[b], (fphase >> b) & 1u);
+        fphase ^= 1u << b;
+        const int64_t xs = x0 + t * tile;
+        const int shift = (t >= ta && t < tb) ? (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2) : 0;
+        j1_compute<WIDE, FULL>(bufs + b * BW + shift, shift == 0, dst, lo, hi, xs, tile, true, ctid, nct);
+        __syncwarp();
+        if ((ctid & 31) == 0) mbar_arrive(&empty[b]);
+        b = b + 1 == S ? 0 : b + 1;
+    }
+}
+
+// blockDim = 32 (producer) + the consumer threads
+__global__ void __launch_bounds__(288) k_jacobi1d_tma(const int *__restrict__ src, int *__restrict__ dst,
                                                      int64_t lo, int64_t hi, int64_t x0, int tile,
                                                      int64_t ntiles, int64_t ta, int64_t tb, int64_t limit,
-                                                     const int *flag, int mode) {
+                                                     int S, const int *flag, int mode) {
     extern __shared__ __align__(128) int smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-    int *bufs = smem + 8;  // 32-byte header: two mbarriers
-    const int64_t t = blockIdx.x;
-    if (t >= ntiles) return;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages;
+    int *bufs = smem + kRingHeader;
+    if ((int64_t)blockIdx.x >= ntiles) return;
+    const int nct = blockDim.x - 32, cwarps = (nct + 31) >> 5;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int j = 0; j < S; j++) {
+            mbar_init(&full[j], 1);
+            mbar_init(&empty[j], cwarps);
+        }
         fence_mbar_init();
-        if (t >= ta && t < tb) j1_issue(src, x0 + t * tile, tile, bufs, &bar[0]);
     }
     __syncthreads();
-    if (narrow_mode(mode, flag))
-        j1_tma_loop<false>(src, dst, lo, hi, x0, tile, t, ntiles, ta, tb, limit, bar, bufs);
+    const int ctid = threadIdx.x - 32;
+    const bool narrow = narrow_mode(mode, flag), full_warps = (nct & 31) == 0;
+    if (threadIdx.x < 32)
+        j1_produce(src, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs);
+    else if (narrow && full_warps)
+        j1_consume<false, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+    else if (narrow)
+        j1_consume<false, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+    else if (full_warps)
+        j1_consume<true, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
     else
-        j1_tma_loop<true>(src, dst, lo, hi, x0, tile, t, ntiles, ta, tb, limit, bar, bufs);
+        j1_consume<true, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
 }
 
 // window: positions [xs-4, xs+tile+4) at shared index pos - xs + 4 (tile % 4 == 0)
@@ -222,7 +256,7 @@ __device__ __forceinline__ void j1_staged_body(const int *__restrict__ src, int 
         }
     }
     __syncthreads();
-    j1_compute<WIDE>(sh, true, dst, lo, hi, xs, tile, vec);
+    j1_compute<WIDE>(sh, true, dst, lo, hi, xs, tile, vec, tid, nt);
 }
 
 __global__ void __launch_bounds__(1024) k_jacobi1d_staged(const int *__restrict__ src,
@@ -300,8 +334,8 @@ struct J2Role {
     unsigned wmask;
 };
 
-__device__ __forceinline__ J2Role j2_role(int TI, int TJ, int qb) {
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+__device__ __forceinline__ J2Role j2_role(int TI, int TJ, int qb, int tid, int nt) {
+    const int lane = tid & 31;
     const int nq = TJ >> 2;
     J2Role r;
     const int groups = nt >= nq ? nt / nq : 1;
@@ -321,7 +355,7 @@ __device__ __forceinline__ J2Role j2_role(int TI, int TJ, int qb) {
 
 // One role's column quad over its rows of the tile at (r0, c0): drow points
 // at dst row r0, columns relative to c0.
-template <bool WIDE>
+template <bool WIDE, bool FULL = false>  // FULL: every warp of the group has 32 lanes
 __device__ __forceinline__ void j2_march(const J2Role &R, const int *base, int pitch, int s0, int ds,
                                          int *__restrict__ drow, int64_t N, int nr, int64_t c0, int64_t J,
                                          bool vec) {
@@ -343,8 +377,8 @@ __device__ __forceinline__ void j2_march(const J2Role &R, const int *base, int p
         sh = (sh + ds) & 3;
         p += sh;
         const int4 dn = live ? lds4(p, sh == 0) : make_int4(0, 0, 0, 0);
-        int l = __shfl_up_sync(R.wmask, cur.w, 1);
-        int r = __shfl_down_sync(R.wmask, cur.x, 1);
+        int l = __shfl_up_sync(FULL ? 0xffffffffu : R.wmask, cur.w, 1);
+        int r = __shfl_down_sync(FULL ? 0xffffffffu : R.wmask, cur.x, 1);
         if (live) {
             if (!R.lin) l = crow[-1];
             if (!R.rin) r = crow[4];
@@ -360,19 +394,35 @@ __device__ __forceinline__ void j2_march(const J2Role &R, const int *base, int p
     }
 }
 
-template <bool WIDE>
+template <bool WIDE, bool FULL = false>  // FULL: every warp of the group has 32 lanes
 __device__ __forceinline__ void j2_compute(const int *base, int pitch, int s0, int ds, int *__restrict__ dst,
                                            int64_t N, int64_t r0, int nr, int64_t c0, int64_t J, int TI, int TJ,
-                                           bool vec) {
-    const int passes = j2_role(TI, TJ, 0).passes;
+                                           bool vec, int tid, int nt) {
+    const int passes = j2_role(TI, TJ, 0, tid, nt).passes;
     for (int qb = 0; qb < passes; qb++)
-        j2_march<WIDE>(j2_role(TI, TJ, qb), base, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, vec);
+        j2_march<WIDE, FULL>(j2_role(TI, TJ, qb, tid, nt), base, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, vec);
 }
 
-// Persistent TMA pipeline for interior 2-D tiles: warp 0 issues one bulk
-// copy per window row (rows start on 16-byte boundaries; the remainder is
-// the row's shift) into the buffer not being computed on.
+// Warp-specialised TMA pipeline for 2-D tiles (same ring as the 1-D one):
+// the producer warp issues one bulk copy per window row (rows start on
+// 16-byte boundaries; the remainder is the row's shift) into window k mod S
+// once the consumer warps have released it.
 constexpr int kRowPad = 16;  // words of slack per window row for the alignment shift
+
+__device__ __forceinline__ uint32_t j2_row_bytes(int TJ, int sh) {
+    return (uint32_t)(((TJ + 8 + sh) * 4 + 15) & ~15);
+}
+
+// true when every rounded window row of the tile lies inside the half
+// [src, src + N*N): only the first column tile of the first row band and the
+// last column tile of the last band can poke out (their extra columns are
+// the neighbouring rows' ends, read but never used)
+__device__ __forceinline__ bool j2_window_ok(const int *src, int64_t N, int64_t r0, int nr, int64_t c0, int TJ) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(src), hi = reinterpret_cast<uintptr_t>(src + N * N);
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
+    const uintptr_t gl = reinterpret_cast<uintptr_t>(src + (r0 + nr) * N + c0 - 4);
+    return (g0 & ~(uintptr_t)15) >= lo && (gl & ~(uintptr_t)15) + j2_row_bytes(TJ, (int)((gl & 15) >> 2)) <= hi;
+}
 
 __device__ __forceinline__ void j2_issue(const int *src, int64_t N, int64_t r0, int nr, int64_t c0, int TJ,
                                          int *buf, int pitch, uint64_t *bar) {
@@ -382,106 +432,117 @@ __device__ __forceinline__ void j2_issue(const int *src, int64_t N, int64_t r0, 
     const int s0 = (int)((a0 & 15) >> 2), ds = (int)(N & 3);
     if (lane == 0) {
         uint32_t total = 0;
-        for (int rr = 0; rr < rows; rr++) total += (uint32_t)(((TJ + 8 + ((s0 + rr * ds) & 3)) * 4 + 15) & ~15);
+        for (int rr = 0; rr < rows; rr++) total += j2_row_bytes(TJ, (s0 + rr * ds) & 3);
         mbar_expect_tx(bar, total);
     }
     __syncwarp();
     for (int rr = lane; rr < rows; rr += 32) {
         const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (r0 - 1 + rr) * N + c0 - 4);
-        const int sh = (int)((ga & 15) >> 2);
-        const uint32_t bytes = (uint32_t)(((TJ + 8 + sh) * 4 + 15) & ~15);
-        tma_load_1d(buf + rr * pitch, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, bar);
+        tma_load_1d(buf + rr * pitch, reinterpret_cast<const void *>(ga & ~(uintptr_t)15),
+                    j2_row_bytes(TJ, (int)((ga & 15) >> 2)), bar);
     }
 }
 
-// Column tiles [ca, cb) are TMA-fed; the edge columns (whose rounded
-// window rows would leave the matrix row) are filled by guarded loads of
-// the whole block from the same persistent loop.
-template <bool WIDE>
-__device__ __forceinline__ void j2_tma_loop(const int *__restrict__ src, int *__restrict__ dst, int64_t N,
-                                            int64_t rlo, int64_t rhi, int64_t J, int TI, int TJ, int64_t ntc,
-                                            int64_t ca, int64_t cb, int64_t t, int64_t t_end, uint64_t *bar,
-                                            int *bufs) {
-    const int pitch = TJ + kRowPad;
-    const int BW = (TI + 2) * pitch;
-    const J2Role role = j2_role(TI, TJ, 0);  // fixed for every tile of this block
-    // Tiles in row-major order (column tile fastest), blocks striding by the
-    // grid: at any moment the whole GPU streams a few full row bands, which
-    // keeps DRAM pages and the halo rows shared with the next band hot.
-    // (Giving each block a contiguous run down a column strip instead
-    // scattered the concurrent streams and measured 3x slower.)
-    const uint32_t ntc32 = (uint32_t)ntc;
-    uint32_t tr = (uint32_t)t / ntc32, tc = (uint32_t)t - tr * ntc32;  // tile -> (row tile, column tile)
-    const uint32_t str = (uint32_t)gridDim.x / ntc32, stc = (uint32_t)gridDim.x - str * ntc32;
-    uint32_t fills[2] = {0u, 0u};  // completed TMA phases per buffer (block-uniform)
-    for (int k = 0; t < t_end; k++, t += gridDim.x) {
-        const int b = k & 1;
-        const int64_t tn = t + gridDim.x;
-        uint32_t trn = tr + str, tcn = tc + stc;
-        if (tcn >= ntc32) {
-            tcn -= ntc32;
-            trn++;
-        }
-        if (threadIdx.x < 32 && tn < t_end && tcn >= ca && tcn < cb) {
-            fence_proxy_async();  // every issuing lane orders the block's earlier reads
-            __syncwarp();
-            const int64_t r0n = rlo + (int64_t)trn * TI, c0n = (int64_t)tcn * TJ;
-            j2_issue(src, N, r0n, (int)min((int64_t)TI, rhi - r0n), c0n, TJ, bufs + (b ^ 1) * BW, pitch,
-                     &bar[b ^ 1]);
-        }
-        const int64_t r0 = rlo + (int64_t)tr * TI, c0 = (int64_t)tc * TJ;
-        const int nr = (int)min((int64_t)TI, rhi - r0);
+// Tiles in row-major order (column tile fastest), blocks striding by the
+// grid: at any moment the whole GPU streams a few full row bands, which
+// keeps DRAM pages and the halo rows shared with the next band hot.
+// (Giving each block a contiguous run down a column strip instead
+// scattered the concurrent streams and measured 3x slower.)
+struct J2Tile {
+    int64_t r0, c0;
+    int nr;
+};
+__device__ __forceinline__ J2Tile j2_tile(int64_t t, int64_t ntc, int64_t rlo, int64_t rhi, int TI, int TJ) {
+    const uint32_t ntc32 = (uint32_t)ntc;  // tile indices < 2^31 (host check)
+    const uint32_t tr = (uint32_t)t / ntc32, tc = (uint32_t)t - tr * ntc32;
+    J2Tile T;
+    T.r0 = rlo + (int64_t)tr * TI;
+    T.c0 = (int64_t)tc * TJ;
+    T.nr = (int)min((int64_t)TI, rhi - T.r0);
+    return T;
+}
+
+__device__ __forceinline__ void j2_produce(const int *__restrict__ src, int64_t N, int64_t rlo, int64_t rhi,
+                                           int TI, int TJ, int64_t ntc, int64_t ntiles, int S, uint64_t *full,
+                                           uint64_t *empty, int *bufs) {
+    const int lane = threadIdx.x & 31;
+    const int pitch = TJ + kRowPad, BW = (TI + 2) * pitch;
+    uint32_t ephase = 0u;  // bit b: parity of empty[b]'s next completion
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&empty[b], ((ephase >> b) & 1u) ^ 1u);  // first S waits pass at once
+        ephase ^= 1u << b;
+        const J2Tile T = j2_tile(t, ntc, rlo, rhi, TI, TJ);
         int *buf = bufs + b * BW;
-        int s0 = 0, ds = 0;
-        if (tc >= ca && tc < cb) {
-            mbar_wait(&bar[b], fills[b] & 1);
-            fills[b]++;
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + (r0 - 1) * N + c0 - 4);
-            s0 = (int)((a0 & 15) >> 2);
-            ds = (int)(N & 3);
+        if (j2_window_ok(src, N, T.r0, T.nr, T.c0, TJ)) {
+            fence_proxy_async();  // earlier generic accesses of buf before the async writes
+            j2_issue(src, N, T.r0, T.nr, T.c0, TJ, buf, pitch, &full[b]);
         } else {
-            for (int e = threadIdx.x; e < (nr + 2) * pitch; e += blockDim.x) {
+            for (int e = lane; e < (T.nr + 2) * pitch; e += 32) {
                 const int rr = e / pitch, cc = e - rr * pitch;
-                const int64_t col = c0 - 4 + cc;
-                buf[e] = (cc < TJ + 8 && col >= 0 && col < N) ? src[(r0 - 1 + rr) * N + col] : 0;
+                const int64_t col = T.c0 - 4 + cc;
+                buf[e] = (cc < TJ + 8 && col >= 0 && col < N) ? src[(T.r0 - 1 + rr) * N + col] : 0;
             }
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[b]);
         }
-        if (role.passes == 1)
-            j2_march<WIDE>(role, buf, pitch, s0, ds, dst + r0 * N + c0, N, nr, c0, J, true);
-        else
-            j2_compute<WIDE>(buf, pitch, s0, ds, dst, N, r0, nr, c0, J, TI, TJ, true);
-        tr = trn;
-        tc = tcn;
-        __syncthreads();
+        b = b + 1 == S ? 0 : b + 1;
     }
 }
 
-__global__ void __launch_bounds__(512) k_jacobi2d_tma(const int *__restrict__ src, int *__restrict__ dst,
+template <bool WIDE>
+__device__ __forceinline__ void j2_consume(const int *__restrict__ src, int *__restrict__ dst, int64_t N,
+                                           int64_t rlo, int64_t rhi, int64_t J, int TI, int TJ, int64_t ntc,
+                                           int64_t ntiles, int S, uint64_t *full, uint64_t *empty, int *bufs,
+                                           int ctid, int nct) {
+    const int pitch = TJ + kRowPad, BW = (TI + 2) * pitch;
+    const J2Role role = j2_role(TI, TJ, 0, ctid, nct);  // fixed for every tile of this block
+    uint32_t fphase = 0u;  // bit b: parity of full[b]'s next completion
+    int b = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const J2Tile T = j2_tile(t, ntc, rlo, rhi, TI, TJ);
+        int s0 = 0, ds = 0;
+        if (j2_window_ok(src, N, T.r0, T.nr, T.c0, TJ)) {
+            s0 = (int)((reinterpret_cast<uintptr_t>(src + (T.r0 - 1) * N + T.c0 - 4) & 15) >> 2);
+            ds = (int)(N & 3);
+        }
+        mbar_wait(&full[b], (fphase >> b) & 1u);
+        fphase ^= 1u << b;
+        const int *buf = bufs + b * BW;
+        if (role.passes == 1)
+            j2_march<WIDE, true>(role, buf, pitch, s0, ds, dst + T.r0 * N + T.c0, N, T.nr, T.c0, J, true);
+        else
+            j2_compute<WIDE, true>(buf, pitch, s0, ds, dst, N, T.r0, T.nr, T.c0, J, TI, TJ, true, ctid, nct);
+        __syncwarp();
+        if ((ctid & 31) == 0) mbar_arrive(&empty[b]);
+        b = b + 1 == S ? 0 : b + 1;
+    }
+}
+
+// blockDim = 32 (producer) + the consumer threads
+__global__ void __launch_bounds__(544) k_jacobi2d_tma(const int *__restrict__ src, int *__restrict__ dst,
                                                       int64_t N, int64_t rlo, int64_t rhi, int64_t J, int TI,
-                                                      int TJ, int64_t ntc, int64_t ca, int64_t cb,
-                                                      int64_t ntiles, const int *flag, int mode) {
+                                                      int TJ, int64_t ntc, int64_t ntiles, int S, const int *flag,
+                                                      int mode) {
     extern __shared__ __align__(128) int smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-    int *bufs = smem + 8;
-    const int64_t t = blockIdx.x, t_end = ntiles;
-    if (t >= t_end) return;
-    const int pitch = TJ + kRowPad;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages;
+    int *bufs = smem + kRingHeader;
+    if ((int64_t)blockIdx.x >= ntiles) return;
+    const int nct = blockDim.x - 32, cwarps = (nct + 31) >> 5;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int j = 0; j < S; j++) {
+            mbar_init(&full[j], 1);
+            mbar_init(&empty[j], cwarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    const int64_t tc = t % ntc;
-    if (threadIdx.x < 32 && tc >= ca && tc < cb) {
-        const int64_t r0 = rlo + (t / ntc) * TI, c0 = tc * TJ;
-        j2_issue(src, N, r0, (int)min((int64_t)TI, rhi - r0), c0, TJ, bufs, pitch, &bar[0]);
-    }
-    if (narrow_mode(mode, flag))
-        j2_tma_loop<false>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, t_end, bar, bufs);
+    if (threadIdx.x < 32)
+        j2_produce(src, N, rlo, rhi, TI, TJ, ntc, ntiles, S, full, empty, bufs);
+    else if (narrow_mode(mode, flag))
+        j2_consume<false>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ntiles, S, full, empty, bufs, threadIdx.x - 32, nct);
     else
-        j2_tma_loop<true>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ca, cb, t, t_end, bar, bufs);
+        j2_consume<true>(src, dst, N, rlo, rhi, J, TI, TJ, ntc, ntiles, S, full, empty, bufs, threadIdx.x - 32, nct);
 }
 
 template <bool WIDE>
@@ -527,7 +588,7 @@ __device__ __forceinline__ void j2_staged_body(const int *__restrict__ src, int 
     }
     __syncthreads();
     (void)lane;
-    j2_compute<WIDE>(sh, pitch, 0, 0, dst, N, r0, nr, c0, J, TI, TJ, vec);
+    j2_compute<WIDE>(sh, pitch, 0, 0, dst, N, r0, nr, c0, J, TI, TJ, vec, threadIdx.x, blockDim.x);
 }
 
 __global__ void __launch_bounds__(1024) k_jacobi2d_staged(const int *__restrict__ src,
@@ -618,6 +679,28 @@ int sweep_mode(const pk_launch_t &L, const int *flag) {
 
 inline int64_t round4(int64_t v) { return (v + 3) & ~(int64_t)3; }
 
+// Ring depth of a TMA pipeline: enough stages that ~24 KB per block is in
+// flight beyond the one being computed on, at most kMaxStages and ~160 KB of
+// shared memory.  PK_TMA_STAGES overrides (tuning sweeps).
+int64_t smem_optin() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return optin;
+}
+
+int tma_stages(size_t stage_bytes) {
+    int S = 1 + (int)((24 * 1024 + stage_bytes - 1) / stage_bytes);
+    if (const char *e = getenv("PK_TMA_STAGES")) {
+        if (atoi(e) > 0) S = atoi(e);
+    }
+    const int cap = (int)((160 * 1024) / stage_bytes);
+    if (S > cap) S = cap;
+    if (S > kMaxStages) S = kMaxStages;
+    if (S < 2) S = 2;
+    return S;
+}
+
 int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int64_t hi,
                  const int *flag, cudaStream_t st) {
     Extents1D e;
@@ -658,10 +741,12 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
             return after_launch("jacobi1d");
         };
         if (tb > ta) {
-            const size_t tsmem = 32 + 2 * ((size_t)tile + kTmaPad) * sizeof(int);
+            const size_t stage = ((size_t)tile + kTmaPad) * sizeof(int);
+            const int S = tma_stages(stage);
+            const size_t tsmem = kRingHeader * sizeof(int) + S * stage;
             rc = allow_smem((const void *)k_jacobi1d_tma, tsmem);
             if (rc) return rc;
-            const int tnt = nt < 256 ? nt : 256;
+            const int tnt = 32 + (nt < 256 ? nt : 256);  // producer warp + consumers
             int per_sm = 0, sms = 148, dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -669,7 +754,7 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
             int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
             if (grid > blocks) grid = blocks;
             k_jacobi1d_tma<<<(unsigned)grid, tnt, tsmem, st>>>(src, dst, lo, hi, x0, tile, blocks, ta, tb, L.N,
-                                                               flag, mode);
+                                                               S, flag, mode);
             return after_launch("jacobi1d_tma");
         }
         return generic(0, blocks);
@@ -706,25 +791,24 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
                 src, dst, L.N, lo, hi, e.J, TI, TJ, tc0, ntc, vec, flag, mode);
             return after_launch("jacobi2d");
         };
-        // column tiles whose rounded window rows lie inside the matrix row
-        // take the TMA pipeline; the edge columns the guarded kernel
-        int64_t ca = (8 + TJ - 1) / TJ, cb = 0;
-        const int64_t room = L.N - 8 - TJ;
-        if (vec && nthreads % 32 == 0 && nthreads <= 512 && room >= 0) cb = room / TJ + 1;
-        if (cb > ntj) cb = ntj;
-        if (cb - ca >= 1) {
-            const size_t tsmem = 32 + 2 * (size_t)(TI + 2) * (size_t)(TJ + kRowPad) * sizeof(int);
+        // the TMA pipeline feeds every tile whose rounded window lies inside
+        // the half (the producer warp fills the rest with guarded loads)
+        const size_t stage = (size_t)(TI + 2) * (size_t)(TJ + kRowPad) * sizeof(int);
+        const int S = tma_stages(stage);
+        const size_t tsmem = kRingHeader * sizeof(int) + S * stage;
+        if (vec && nthreads % 32 == 0 && nthreads <= 512 && (int64_t)tsmem <= smem_optin()) {
             rc = allow_smem((const void *)k_jacobi2d_tma, tsmem);
             if (rc) return rc;
+            const int tnt = 32 + (int)nthreads;  // producer warp + consumers
             int per_sm = 0, sms = 148, dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi2d_tma, (int)nthreads, tsmem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi2d_tma, tnt, tsmem);
             const int64_t ntiles = nti * ntj;
             int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
             if (grid > ntiles) grid = ntiles;
-            k_jacobi2d_tma<<<(unsigned)grid, (unsigned)nthreads, tsmem, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ,
-                                                                             ntj, ca, cb, ntiles, flag, mode);
+            k_jacobi2d_tma<<<(unsigned)grid, (unsigned)tnt, tsmem, st>>>(src, dst, L.N, lo, hi, e.J, TI, TJ, ntj,
+                                                                        ntiles, S, flag, mode);
             return after_launch("jacobi2d_tma");
         }
         return generic(0, ntj);
