@@ -87,6 +87,7 @@ class CaseTable:
     cases: tuple[Case, ...]
     source: str
     tree: dict
+    counters: tuple[dict, ...] = ()
 
     def machine_names(self) -> tuple[str, ...]:
         return tuple(p["name"] for p in self.machine_params)
@@ -130,6 +131,7 @@ def _load(path: str) -> CaseTable:
         tuple(cases),
         doc["source"],
         doc.get("tree", {}),
+        tuple(doc.get("counters", ())),
     )
 
 
@@ -181,7 +183,17 @@ def select(kind_or_family, params: dict, machine=None) -> Selection:
     if missing:
         raise KeyError("no value supplied for parameter %r" % missing[0])
     for name in tab.machine_names():
+        if name not in mv.values:
+            raise KeyError("machine model %r needs a value for %r" % (mv.table, name))
         assignment[name] = Fraction(mv.values[name])
+    for c in tab.counters:
+        # the occupancy counter's warp_slots is a number baked into the table;
+        # it must be the device's resident-warp count for the table to apply
+        if c.get("measure") == "occupancy":
+            built, have = int(c["options"].get("warp_slots", 48)), machine_mod.warp_slots(mv)
+            if have is not None and have != built:
+                raise ValueError("case table %s.%s assumes %d warp slots per SM; device %s has %d"
+                                 % (family, mv.table, built, mv.source, have))
     hold = tab.holding(assignment)
     if len(hold) > 1:  # the leaves partition the box; keep the first (tree order) if not
         hold = hold[:1]

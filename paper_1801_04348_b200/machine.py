@@ -13,11 +13,18 @@ discussion come from ``cudaGetDeviceProperties`` through the C ABI
 
 The warp size (32) is not one of the reference's machine parameters; the
 tuner applies it as an executor-side filter.
+
+Occupancy model (data/b200-occ.machine): the reference's
+``occupancy`` performance counter (counters.py:512-524) with its register
+file bound to the live ``regsPerMultiprocessor`` (R_F) and its warp slots
+to ``maxThreadsPerMultiProcessor / warpSize`` (64 on sm_100; the reference
+defaults to 48); the target O in [0, 1] is the caller's.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from fractions import Fraction
 from functools import lru_cache
 
 from . import _lib
@@ -36,6 +43,8 @@ B200_NOMINAL = {
     "smem_per_block": 49152,
     "smem_per_block_optin": 232448,
     "l2_bytes": 126 * 1024 * 1024,
+    "regs_per_sm": 65536,
+    "max_threads_per_sm": 2048,
 }
 
 
@@ -43,8 +52,8 @@ B200_NOMINAL = {
 class MachineValues:
     """Values for the machine parameters of one case-table machine model."""
 
-    table: str  # which case tables to evaluate: 'b200' | 'fermi'
-    values: dict  # Z_B, R_B, T_B
+    table: str  # which case tables to evaluate: 'b200' | 'b200-occ' | 'fermi'
+    values: dict  # Z_B, R_B, T_B (+ R_F, O for 'b200-occ')
     source: str  # 'live:<device>' | 'fermi.machine' | 'nominal' | 'user'
     props: dict = field(default_factory=dict, compare=False)
     warp_size: int = 32
@@ -64,20 +73,41 @@ def _live_props(device: int) -> tuple:
     return tuple(sorted(_lib.query_machine(device).items()))
 
 
-def live(device: int = 0, smem: str = "optin") -> MachineValues:
-    """Query the device (pk_query_machine) -- replaces the machine constants."""
+def _with_occupancy(mv: MachineValues, occupancy) -> MachineValues:
+    """The same device on the occupancy model: R_F from the live register
+    file, O = the requested target (a ratio in [0, 1])."""
+    target = Fraction(occupancy)
+    if not 0 <= target <= 1:
+        raise ValueError("occupancy target O must lie in [0, 1], got %s" % occupancy)
+    values = dict(mv.values, R_F=int(mv.props["regs_per_sm"]), O=target)
+    return MachineValues("b200-occ", values, mv.source, mv.props, mv.warp_size)
+
+
+def live(device: int = 0, smem: str = "optin", occupancy=None) -> MachineValues:
+    """Query the device (pk_query_machine) -- replaces the machine constants.
+    ``occupancy``: evaluate the occupancy model with this target O."""
     props = dict(_live_props(device))
     if props.get("cc_major") != 10:
         raise RuntimeError(
             "device %d is sm_%d%d; libpk is built for sm_100a only"
             % (device, props.get("cc_major"), props.get("cc_minor"))
         )
-    return MachineValues("b200", values_from_props(props, smem), "live:%d" % device, props,
-                         int(props["warp_size"]))
+    mv = MachineValues("b200", values_from_props(props, smem), "live:%d" % device, props,
+                       int(props["warp_size"]))
+    return mv if occupancy is None else _with_occupancy(mv, occupancy)
 
 
-def nominal(smem: str = "optin") -> MachineValues:
-    return MachineValues("b200", values_from_props(B200_NOMINAL, smem), "nominal", dict(B200_NOMINAL))
+def nominal(smem: str = "optin", occupancy=None) -> MachineValues:
+    mv = MachineValues("b200", values_from_props(B200_NOMINAL, smem), "nominal", dict(B200_NOMINAL))
+    return mv if occupancy is None else _with_occupancy(mv, occupancy)
+
+
+def warp_slots(mv: MachineValues) -> int | None:
+    """Resident warps per SM of the device behind ``mv`` (None if unknown)."""
+    p = mv.props
+    if "max_threads_per_sm" in p and p.get("warp_size"):
+        return int(p["max_threads_per_sm"]) // int(p["warp_size"])
+    return None
 
 
 def fermi() -> MachineValues:
@@ -96,7 +126,7 @@ def resolve(machine=None) -> MachineValues:
     if machine == "static":
         return live(smem="static")
     if isinstance(machine, dict):
-        return MachineValues("b200", dict(machine), "user")
+        return MachineValues("b200-occ" if "O" in machine else "b200", dict(machine), "user")
     raise ValueError("unknown machine %r" % (machine,))
 
 

@@ -91,3 +91,56 @@ def test_machine_file_text_parses_with_reference_syntax():
     cp.read_string(text)
     assert cp["param.Z_B"]["range"] == "0 58112"
     assert cp["counter.threads"]["bound"] == "T_B"
+
+
+# ---- occupancy model (data/b200-occ.machine) -----------------
+
+OCC_FAMILIES = ("addition", "jacobi", "jacobi2d", "matmul", "matvec", "reverse", "transpose")
+
+
+def test_occupancy_tables_carry_the_counter():
+    for fam in OCC_FAMILIES:
+        tab = cases.table(fam, "b200-occ")
+        assert {"R_F", "O"} <= set(tab.machine_names())
+        (occ,) = [c for c in tab.counters if c["measure"] == "occupancy"]
+        assert occ["bound"] == "O" and occ["options"]["register_file"] == "R_F"
+        assert int(occ["options"]["warp_slots"]) == 64  # 2048 threads / 32 per SM on sm_100
+        # the counter only restricts: same leaves (applied tuples) as the b200 table
+        assert [c.applied for c in tab.cases] == [c.applied for c in cases.table(fam, "b200").cases]
+        for c in tab.cases:
+            assert any("R_F" in k.text and "O" in k.text for k in c.constraints)
+
+
+def test_occupancy_constraint_is_the_reference_ratio():
+    # counters.py:512-524: R_F / (threads * regs * warp_slots) <= O, regs = the
+    # case program's peak live registers (10 for the original 1-D Jacobi)
+    from fractions import Fraction
+
+    mv0 = machine.nominal(occupancy=1)
+    for B in (64, 96, 102, 103, 128, 256, 1024):
+        for O in (Fraction(1), Fraction(1, 2), Fraction(1, 5)):
+            mv = machine.MachineValues("b200-occ", dict(mv0.values, O=O), "user", mv0.props)
+            sel = cases.select("jacobi", {"T": 4, "N": 4098, "s": 2, "B": B}, mv)
+            ratio = Fraction(65536, B * 10 * 64)
+            assert (not sel.fallback and sel.index == 1) == (ratio <= O), (B, O)
+
+
+def test_occupancy_selection_refines_b200():
+    mv_occ, mv = machine.nominal(occupancy=1), machine.nominal()
+    P = {"n": 8192, "B0": 128, "ub1": 8, "s": 16}
+    assert cases.select("matmul", P, mv_occ).index == cases.select("matmul", P, mv).index == 1
+    # a 64-thread reversal block cannot reach the ratio on a 64K register file
+    sel = cases.select("reverse", {"N": 1 << 20, "s": 16, "B": 64}, mv_occ)
+    assert sel.fallback
+
+
+def test_occupancy_target_range_and_warp_slots_checked():
+    with pytest.raises(ValueError):
+        machine.nominal(occupancy=2)
+    mv = machine.nominal(occupancy=1)
+    odd = machine.MachineValues("b200-occ", mv.values, "user", dict(mv.props, max_threads_per_sm=1536))
+    with pytest.raises(ValueError, match="warp slots"):
+        cases.select("jacobi", {"T": 4, "N": 4098, "s": 2, "B": 256}, odd)
+    with pytest.raises(KeyError):
+        cases.select("jacobi", {"T": 4, "N": 4098, "s": 2, "B": 256},
+                     machine.MachineValues("b200-occ", machine.nominal().values, "user"))

@@ -31,3 +31,22 @@ def test_temporal_jacobi1d_wide_values(cuda, oracle_mod):
     want = oracle_mod.run("jacobi", params, {"a": a})["a"]
     got = run_program(programs.source("jacobi"), params, {"a": a}, temporal=5)["a"]
     assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+
+
+def test_occupancy_model_on_live_device(cuda, oracle_mod):
+    """The occupancy counter's register file is the live regsPerMultiprocessor
+    and its warp slots the live resident-warp count; selection on that model
+    drives the same kernels."""
+    from paper_1801_04348_b200 import interp, machine, programs, run_program
+
+    mv = machine.live(occupancy=1)
+    assert mv.table == "b200-occ" and mv.values["R_F"] == mv.props["regs_per_sm"] == 65536
+    assert machine.warp_slots(mv) == 64
+    rng = np.random.default_rng(7)
+    params = {"T": 5, "N": 8194, "s": 4, "B": 256}
+    a = rng.integers(-1000, 1000, size=2 * params["N"]).astype(np.int32)
+    want = oracle_mod.run("jacobi", params, {"a": a})["a"]
+    got = run_program(programs.source("jacobi"), params, {"a": a}, machine=mv)["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+    info = interp.last_run()
+    assert info.case == 1 and not info.fallback

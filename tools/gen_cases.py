@@ -62,6 +62,7 @@ def build(ref_src: str) -> dict:
         "fermi.machine": load_machine(os.path.join(ref_data, "fermi.machine")),
         "addition.machine": load_machine(os.path.join(ref_data, "addition.machine")),
         "b200.machine": load_machine(os.path.join(PKG_DATA, "b200.machine")),
+        "b200-occ.machine": load_machine(os.path.join(PKG_DATA, "b200-occ.machine")),
     }
     out = {}
     for fam, (prog_ref, default_machine) in FAMILIES.items():
@@ -69,7 +70,7 @@ def build(ref_src: str) -> dict:
         base = ref_data if where == "ref" else os.path.join(PKG_DATA, "programs")
         with open(os.path.join(base, fname)) as fh:
             program = dsl.parse(fh.read())
-        for mfile in (default_machine, "b200.machine"):
+        for mfile in (default_machine, "b200.machine", "b200-occ.machine"):
             machine = machines[mfile]
             result = engine.optimize(program, machine)
             order = result.order
@@ -107,6 +108,11 @@ def build(ref_src: str) -> dict:
                 "machine_params": [
                     {"name": p.name, "kind": p.kind, "lo": str(p.lo), "hi": str(p.hi)}
                     for p in machine.params
+                ],
+                "counters": [
+                    {"name": c.name, "measure": c.measure, "bound": c.bound, "kind": c.kind,
+                     "options": dict(c.options)}
+                    for c in machine.counters
                 ],
                 "box": {k: [str(v[0]), str(v[1])] for k, v in result.box.items()},
                 "decision_height": result.tree.height(),
