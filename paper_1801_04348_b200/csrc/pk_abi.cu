@@ -230,6 +230,33 @@ int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void 
     return jacobi_narrow(*L, a, narrow, static_cast<cudaStream_t>(stream));
 }
 
+namespace {
+
+constexpr int kMaxChunks = 8;                  // pipeline depth limit of pk_run_host
+constexpr int64_t kChunkBytes = 48ll << 20;    // PCIe bytes per chunk (~1 ms of transfer)
+
+// Units (rows, or elements for reversal) a host-buffer run may be cut into:
+// families whose unit ranges touch disjoint slices of the streamed arrays.
+// The stencils are not chunked (every step needs the whole array).
+bool chunkable(const pk_launch_t &L) {
+    switch (L.family) {
+        case PK_FAMILY_REVERSE:
+        case PK_FAMILY_TRANSPOSE:
+        case PK_FAMILY_MATVEC:
+        case PK_FAMILY_MATMUL:
+        case PK_FAMILY_ADDITION: return true;
+        default: return false;
+    }
+}
+
+struct HostRun {
+    cudaStream_t h2d = nullptr, d2h = nullptr, cs[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2 * kMaxChunks] = {};
+    void *dev[3] = {nullptr, nullptr, nullptr};
+};
+
+}  // namespace
+
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device) {
     int rc = validate(L, nptrs);
     if (rc) return rc;
@@ -237,44 +264,116 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     array_spec(*L, &spec);
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
-    cudaStream_t st;
-    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
-    void *dev[3] = {nullptr, nullptr, nullptr};
+
+    // Cut the unit range into chunks so PCIe runs under the kernels: chunk k's
+    // operands go up on the h2d stream while chunk k-1 computes (two compute
+    // streams, so a chunk's kernel fills the previous one's tail) and chunk
+    // k-2's results come down on the d2h stream.  Operands every chunk needs
+    // whole (matmul's b, mat-vec's x, transpose's a) go up once, first.
+    const int64_t N = L->N > 0 ? L->N : 0;
+    const int64_t u0 = L->hi > 0 ? (L->lo > 0 ? L->lo : 0) : 0, u1 = L->hi > 0 ? L->hi : N;
+    int64_t unit_bytes = 0;  // streamed bytes per unit
+    for (int i = 0; i < spec.count; i++) unit_bytes += (spec.written[i] ? 2 : 1) * (spec.elems[i] / (N > 0 ? N : 1)) * 4;
+    int nchunks = 1;
+    if (chunkable(*L) && u1 > u0 && unit_bytes > 0) {
+        const int64_t total = (u1 - u0) * unit_bytes;
+        nchunks = (int)(total / kChunkBytes);
+        if (nchunks > kMaxChunks) nchunks = kMaxChunks;
+        if (nchunks < 1) nchunks = 1;
+    }
+    int64_t step = (u1 - u0 + nchunks - 1) / nchunks;
+    const int64_t align = L->family == PK_FAMILY_REVERSE ? 4096 : 128;  // whole tiles per chunk
+    step = (step + align - 1) / align * align;
+    if (step < 1) step = 1;
+    nchunks = (int)((u1 - u0 + step - 1) / step);
+    if (nchunks < 1) nchunks = 1;
+
+    HostRun R;
     rc = PK_OK;
+    e = cudaStreamCreateWithFlags(&R.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[0], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[1], cudaStreamNonBlocking);
+    for (int k = 0; k < 2 * nchunks && e == cudaSuccess; k++) e = cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming);
+    if (e != cudaSuccess) rc = fail(PK_E_CUDA, "stream/event setup: %s", cudaGetErrorString(e));
+
+    auto chunk = [&](int k) {
+        pk_launch_t C = *L;
+        if (nchunks > 1 || L->hi > 0) {
+            C.lo = u0 + k * step;
+            C.hi = u0 + (k + 1) * step < u1 ? u0 + (k + 1) * step : u1;
+        }
+        return C;
+    };
+    bool whole[3] = {false, false, false};  // needed whole by every chunk: moved once
     for (int i = 0; i < spec.count && rc == PK_OK; i++) {
         const size_t bytes = (size_t)spec.elems[i] * 4;
-        e = scratch_alloc(&dev[i], bytes, st);
+        e = scratch_alloc(&R.dev[i], bytes, R.h2d);
         if (e != cudaSuccess) {
             rc = fail(PK_E_ALLOC, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
             break;
         }
         int64_t off, cnt;
-        array_range(*L, i, spec.elems[i], &off, &cnt);
-        char *d = static_cast<char *>(dev[i]) + off * 4;
-        if (cnt && host_ptrs[i]) {
-            e = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * 4, (size_t)cnt * 4,
-                                cudaMemcpyHostToDevice, st);
-            if (e != cudaSuccess) rc = fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(e));
-        } else if (cnt) {
-            cudaMemsetAsync(d, 0, (size_t)cnt * 4, st);  // missing arrays are zero-filled (interp.py:79-81)
-        }
+        array_range(chunk(0), i, spec.elems[i], &off, &cnt);
+        whole[i] = nchunks == 1 || (off == 0 && cnt == spec.elems[i]);
     }
-    if (rc == PK_OK) rc = dispatch(*L, dev, st);
-    for (int i = 0; i < spec.count && rc == PK_OK; i++) {
+    auto up = [&](const pk_launch_t &C, int i) -> int {
         int64_t off, cnt;
-        array_range(*L, i, spec.elems[i], &off, &cnt);
-        if (spec.written[i] && cnt && host_ptrs[i]) {
-            e = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * 4, static_cast<char *>(dev[i]) + off * 4,
-                                (size_t)cnt * 4, cudaMemcpyDeviceToHost, st);
-            if (e != cudaSuccess) rc = fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(e));
+        array_range(C, i, spec.elems[i], &off, &cnt);
+        char *d = static_cast<char *>(R.dev[i]) + off * 4;
+        if (cnt && host_ptrs[i]) {
+            cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * 4, (size_t)cnt * 4,
+                                            cudaMemcpyHostToDevice, R.h2d);
+            if (x != cudaSuccess) return fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(x));
+        } else if (cnt) {
+            cudaMemsetAsync(d, 0, (size_t)cnt * 4, R.h2d);  // missing arrays are zero-filled (interp.py:79-81)
         }
+        return PK_OK;
+    };
+    auto down = [&](const pk_launch_t &C, int i) -> int {
+        int64_t off, cnt;
+        array_range(C, i, spec.elems[i], &off, &cnt);
+        if (!spec.written[i] || !cnt || !host_ptrs[i]) return PK_OK;
+        cudaError_t x = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * 4,
+                                        static_cast<char *>(R.dev[i]) + off * 4, (size_t)cnt * 4,
+                                        cudaMemcpyDeviceToHost, R.d2h);
+        return x == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(x));
+    };
+    for (int i = 0; i < spec.count && rc == PK_OK; i++)
+        if (whole[i]) rc = up(nchunks == 1 ? *L : chunk(0), i);
+    for (int k = 0; k < nchunks && rc == PK_OK; k++) {
+        const pk_launch_t C = chunk(k);
+        for (int i = 0; i < spec.count && rc == PK_OK; i++)
+            if (!whole[i]) rc = up(C, i);
+        if (rc) break;
+        cudaEventRecord(R.ev[2 * k], R.h2d);
+        cudaStream_t cs = R.cs[k & 1];
+        cudaStreamWaitEvent(cs, R.ev[2 * k], 0);
+        rc = dispatch(C, R.dev, cs);
+        if (rc) break;
+        cudaEventRecord(R.ev[2 * k + 1], cs);
+        cudaStreamWaitEvent(R.d2h, R.ev[2 * k + 1], 0);
+        for (int i = 0; i < spec.count && rc == PK_OK; i++)
+            if (!whole[i] || nchunks == 1) rc = down(C, i);
     }
+    // written operands moved whole come down after the last chunk (none of
+    // the chunked families writes one; kept for completeness)
+    for (int i = 0; i < spec.count && rc == PK_OK; i++)
+        if (whole[i] && nchunks > 1) rc = down(*L, i);
+    cudaError_t se = cudaSuccess;
+    for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h}) {
+        if (!s) continue;
+        cudaError_t x = cudaStreamSynchronize(s);
+        if (se == cudaSuccess) se = x;
+    }
+    if (se != cudaSuccess && rc == PK_OK) rc = fail(PK_E_CUDA, "kernel execution: %s", cudaGetErrorString(se));
     for (int i = 0; i < spec.count; i++)
-        if (dev[i]) cudaFreeAsync(dev[i], st);
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess && rc == PK_OK) rc = fail(PK_E_CUDA, "kernel execution: %s", cudaGetErrorString(e));
-    cudaStreamDestroy(st);
+        if (R.dev[i]) cudaFreeAsync(R.dev[i], R.d2h);
+    if (R.d2h) cudaStreamSynchronize(R.d2h);
+    for (int k = 0; k < 2 * kMaxChunks; k++)
+        if (R.ev[k]) cudaEventDestroy(R.ev[k]);
+    for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h})
+        if (s) cudaStreamDestroy(s);
     return rc;
 }
 

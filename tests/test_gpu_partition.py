@@ -130,3 +130,46 @@ def test_run_host_shares_reassemble_oracle(cuda, oracle_mod, family, params):
         _lib.run_host(L, [host[a.name].ctypes.data for a in programs.FAMILIES[family].arrays], 0)
     for name in programs.FAMILIES[family].written:
         assert np.array_equal(host[name].reshape(-1), np.asarray(want[name]).reshape(-1)), name
+
+
+@pytest.mark.parametrize("family,params,share", [
+    ("matmul", {"n": 4096, "B0": 128, "ub1": 8, "s": 16}, None),
+    ("matmul", {"n": 4096, "B0": 128, "ub1": 8, "s": 16}, (1000, 3001)),
+    ("reverse", {"N": 1 << 25, "s": 16, "B": 256}, None),
+    ("reverse", {"N": 1 << 25, "s": 16, "B": 256}, (12345, 30000000)),
+    ("matvec", {"N": 8192, "s": 1, "B": 256}, None),
+    ("transpose", {"N": 4096, "s": 8, "B0": 64, "B1": 8}, None),
+    ("addition", {"N": 4096, "B0": 4, "B1": 64}, None),
+])
+def test_run_host_pipeline_matches_device_launch(cuda, family, params, share):
+    """Large host-buffer runs are cut into row chunks whose PCIe traffic
+    overlaps the kernels; the result equals one pk_launch on device buffers."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, binding, cases, programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    f32 = family in ("matmul", "matvec")
+    rng = np.random.default_rng(11)
+    init = {}
+    for k, s in shapes.items():
+        if f32:
+            init[k] = rng.uniform(-1, 1, size=s).astype(np.float32)
+        else:
+            init[k] = rng.integers(-1000, 1000, size=s).astype(np.int32)
+    sel = cases.select(kind, params, "nominal")
+    dtype = _lib.DTYPE_F32 if f32 else _lib.DTYPE_I32
+    lo, hi = share if share else (0, 0)
+    L = binding.make_launch(kind, params, sel.applied, dtype, lo=lo, hi=hi)
+    names = [a.name for a in programs.FAMILIES[family].arrays]
+    dev = [torch.from_numpy(init[n].reshape(-1).copy()).cuda() for n in names]
+    _lib.launch(L, [t.data_ptr() for t in dev], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    host = {n: np.ascontiguousarray(init[n].copy()) for n in names}
+    _lib.run_host(L, [host[n].ctypes.data for n in names], 0)
+    for n, t in zip(names, dev):
+        if n in programs.FAMILIES[family].written:
+            # outside a share both sides keep the initial contents
+            want = t.cpu().numpy().reshape(-1)
+            assert np.array_equal(host[n].reshape(-1).view(np.int32), want.view(np.int32)), n
