@@ -129,7 +129,10 @@ int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stre
  * (L->hi > 0) only the rank's share crosses PCIe: the rows of row-sharded
  * operands (matmul a/c, mat-vec a/y, transpose c, addition), the mirrored
  * range for reversal; replicated operands (b, x, transpose's a) and the
- * stencil buffers are copied whole. */
+ * stencil buffers are copied whole.  Large runs of the row-sharded families
+ * are cut into up to 8 unit chunks (~48 MB of PCIe traffic each) pipelined
+ * over an H2D stream, two compute streams and a D2H stream, so the copies
+ * overlap the kernels; results are identical to one pk_launch. */
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device);
 
 /* One Jacobi sweep over an explicit position range, used by the slab
