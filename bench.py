@@ -1,7 +1,7 @@
 """bench.py -- the driver's benchmark contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload matmul8192|matmul2048|matmul1024|jacobi|jacobi2d|reverse|transpose|matvec]
+                    [--n 8192] [--no-kernels] [--no-cpu] [--no-tune] [--e2e-steps E]
 
 Headline workload (BASELINE.json configs[1]): FP32 matrix multiplication
 n = 8192, program parameters auto-tuned inside the case the live B200
@@ -34,6 +34,24 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
+NCU_TRAFFIC = os.path.join(REPO, "profiles", "ncu_traffic.json")
+# which committed ncu capture describes each measured kernel (tools/make_profiles.py)
+TRAFFIC_KEYS = {"matmul": "matmul_n8192", "reverse": "reverse_2p30", "transpose": "transpose_32768",
+                "jacobi": "jacobi1d_2p28", "jacobi2d": "jacobi2d_16384", "matvec": "matvec_32768"}
+
+
+def ncu_traffic(key: str):
+    """DRAM bytes (read + write) per launch of the kernel captured under
+    ``key`` by one ``ncu --set full`` run (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(NCU_TRAFFIC) as fh:
+            rec = json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None
+    return None if rec is None else {"bytes": rec["dram_bytes"], "kernel": rec["kernel"].split("(")[0],
+                                     "report": "profiles/%s_ncu.md (%s)" % (rec["round"], rec["report"])}
+
+
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 METRIC = "matmul GFLOP/s & stencil/reversal HBM GB/s, case-selected kernels, 1/2/4/8 B200"
 
@@ -198,6 +216,9 @@ def main() -> int:
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-family extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-tune", action="store_true",
+                    help="skip the tuners and use each grid's first entry (the recorded picks); "
+                         "for profiler runs, whose timings are distorted")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -234,7 +255,10 @@ def main() -> int:
     # tune (B0, ub1, s) inside the selected case, on this rank's shard
     grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in
             ((128, 8, 16), (128, 8, 8), (64, 8, 16), (64, 8, 8), (64, 16, 8))]
-    tuned, trials = autotune.autotune(kind, base, machine=mv, buffers=[a, b, c], reps=2, grid=grid)
+    if args.no_tune:  # profiler runs: timings under ncu are distorted, use the recorded pick
+        tuned, trials = dict(base, **grid[0]), []
+    else:
+        tuned, trials = autotune.autotune(kind, base, machine=mv, buffers=[a, b, c], reps=2, grid=grid)
     sel = cases.select(kind, tuned, mv)
     L = binding.make_launch(kind, tuned, sel.applied, _lib.DTYPE_F32, lo=r0, hi=r0 + rows)
     stream = torch.cuda.current_stream(dev)
@@ -272,6 +296,13 @@ def main() -> int:
     peak_tf = sm_count * 256 * peaks["sm_max_mhz"] * 1e6 / 1e12
     clocks = clk.summary()
     peak_at_clock = sm_count * 256 * clocks["sm_mhz"] * 1e6 / 1e12 if clocks["sm_mhz"] else None
+
+    # DRAM traffic of the dominant kernel per launch, from the committed ncu
+    # capture of this exact configuration (one rank, the TMA-fed 128 x 128 leaf)
+    headline_traffic = None
+    if world == 1 and n == 8192 and (tuned["B0"], tuned["ub1"], tuned["s"]) == (128, 8, 16):
+        rec = ncu_traffic(TRAFFIC_KEYS["matmul"])
+        headline_traffic = rec["bytes"] if rec else None
 
     # e2e through the C-ABI host-buffer call (pinned host memory)
     e2e = None
@@ -327,7 +358,7 @@ def main() -> int:
     cpu = None
     if rank == 0 and world == 1 and not args.no_kernels:
         del ha, hb, hc
-        kernels = bench_kernels(peaks, mv)
+        kernels = bench_kernels(peaks, mv, args.no_tune)
         try:
             kernels["emitted_baseline"] = bench_emitted(kernels)
         except Exception as exc:  # the baseline is informative only
@@ -355,7 +386,7 @@ def main() -> int:
                          "peak_source": "computed: %d SM x 256 FLOP/clk x %.0f MHz max clock "
                                         "(MEASURED_PEAKS.json has no FP32 figure)" % (sm_count, peaks["sm_max_mhz"]),
                          "frac_at_observed_clock": round(achieved_tf / peak_at_clock, 4) if peak_at_clock else None,
-                         "traffic": None},
+                         "traffic": headline_traffic},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -371,7 +402,7 @@ def main() -> int:
     return 0
 
 
-def bench_kernels(peaks, mv) -> dict:
+def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
     """The bandwidth-bound BASELINE configs on one GPU: GB/s of algorithmic
     traffic and the fraction of the measured copy bandwidth."""
     import torch
@@ -393,8 +424,11 @@ def bench_kernels(peaks, mv) -> dict:
         ptrs = [x.data_ptr() for x in bufs]
         # tune (B, s) / (B0, B1, s) inside the live case on 2 time steps, run the full T
         tune_base = dict(params, T=2) if "T" in params else dict(params)
-        tuned, trials = autotune.autotune(kind, tune_base, machine=mv, buffers=bufs, reps=2,
-                                          grid=TUNE_GRIDS.get(fam))
+        if no_tune:
+            tuned, trials = dict(tune_base, **TUNE_GRIDS[fam][0]), []
+        else:
+            tuned, trials = autotune.autotune(kind, tune_base, machine=mv, buffers=bufs, reps=2,
+                                              grid=TUNE_GRIDS.get(fam))
         run_params = dict(tuned, T=params["T"]) if "T" in params else tuned
         sel = cases.select(kind, run_params, mv)
         L = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32)
@@ -413,6 +447,13 @@ def bench_kernels(peaks, mv) -> dict:
         out[fam] = {"params": run_params, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
                     "value": round(gbs, 1), "unit": unit, "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
                     "frac_of_8tbs": round(gbs / 8000.0, 4), "tuning_trials": len(trials)}
+        rec = ncu_traffic(TRAFFIC_KEYS[fam])
+        if rec and run_params == dict(params, **TUNE_GRIDS[fam][0]):
+            # per launch (per sweep for the stencils) from the committed ncu capture
+            per = (work / params["T"]) if "T" in params else work
+            out[fam]["traffic"] = {"dram_bytes": rec["bytes"], "algorithmic_bytes": per,
+                                   "ratio": round(rec["bytes"] / per, 4), "kernel": rec["kernel"],
+                                   "source": rec["report"]}
         if fam == "jacobi":  # temporally blocked variant, reported separately (same results)
             for h in (7, 15):
                 Lt = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32,
@@ -486,14 +527,15 @@ def bench_emitted(ours: dict) -> dict:
 
 
 # candidate program parameters per family (warp-multiple blocks; coverage-preserving
-# ones are kept by the tuner)
+# ones are kept by the tuner).  The first entry of each grid is the tuner's pick on
+# B200 in the last measured run (profiles/r01*_bench.json), used by --no-tune.
 TUNE_GRIDS = {
     "reverse": [{"B": b, "s": s} for b, s in ((256, 16), (128, 32), (512, 8), (1024, 4), (256, 8))],
     "transpose": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((64, 8, 8), (32, 8, 4), (64, 16, 4),
                                                                  (32, 32, 1), (128, 8, 4))],
     "jacobi": [{"B": b, "s": s} for b, s in ((256, 16), (256, 8), (128, 32), (512, 8), (1024, 4))],
-    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((32, 8, 32), (64, 4, 32), (32, 8, 16),
-                                                                (8, 32, 16), (16, 16, 32))],
+    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((8, 32, 16), (32, 8, 32), (64, 4, 32),
+                                                                (32, 8, 16), (16, 16, 32))],
     "matvec": [{"B": b, "s": s} for b, s in ((256, 1), (128, 1), (64, 2), (512, 1), (32, 4))],
 }
 

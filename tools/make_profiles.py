@@ -1,10 +1,13 @@
-"""Write profiles/<round>_ncu.md from ncu reports and a launch list.
+"""Write profiles/<round>_ncu.md from ncu reports and a launch list, and
+profiles/ncu_traffic.json (DRAM bytes per launch of each captured kernel,
+read by bench.py for roofline.traffic).
 
 python tools/make_profiles.py r01 gpurun_out/launches.csv name=path.ncu-rep [...]
 """
 
 import csv
 import io
+import json
 import os
 import sys
 
@@ -51,13 +54,25 @@ def launches_table(path):
     return "\n".join(out)
 
 
+def to_bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    return float(v.replace(",", "")) * scale.get(unit, 1)
+
+
+def to_us(v, unit):
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+    return float(v.replace(",", "")) * scale.get(unit, 1.0)
+
+
 def main():
     rnd, launches = sys.argv[1], sys.argv[2]
     reps = [a.split("=", 1) for a in sys.argv[3:]]
     lines = ["# ncu evidence, round %s" % rnd, "",
              "Captured on one B200 with `ncu --set full --clock-control none --import-source on`"
              " (one launch per report, cold caches, serialised); launch list with"
-             " `--metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 1`."
+             " `--metrics gpu__time_duration.sum --clock-control none` over"
+             " `bench.py --steps 3 --warmup 3 --no-cpu --no-tune` (the tuners' recorded picks: timings"
+             " under a profiler would mislead them)."
              " Numbers from a profiled run are evidence, never bench values.", ""]
     if os.path.exists(launches):
         lines += ["## Launch list of the bench command (share of device time)", "", launches_table(launches), ""]
@@ -71,6 +86,19 @@ def main():
                     lines.append("| %s | %s %s |" % (k, v, u))
         lines.append("")
     os.makedirs("profiles", exist_ok=True)
+    traffic = {}
+    for name, path in reps:
+        for kern in summary(path):
+            rd, wr = kern.get("dram__bytes_read.sum"), kern.get("dram__bytes_write.sum")
+            t = kern.get("gpu__time_duration.sum")
+            if rd and wr:
+                traffic[name] = {"kernel": kern.get("Kernel Name", ("?", ""))[0][:120],
+                                 "dram_bytes": to_bytes(*rd) + to_bytes(*wr),
+                                 "gpu_time_us": to_us(*t) if t else None,
+                                 "report": os.path.basename(path), "round": rnd}
+    with open(os.path.join("profiles", "ncu_traffic.json"), "w") as fh:
+        json.dump(traffic, fh, indent=1, sort_keys=True)
+        fh.write("\n")
     out = os.path.join("profiles", "%s_ncu.md" % rnd)
     with open(out, "w") as fh:
         fh.write("\n".join(lines) + "\n")

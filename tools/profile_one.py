@@ -1,6 +1,6 @@
 """Launch one family's case-selected kernel a few times (for ncu captures).
 
-python tools/profile_one.py FAMILY '{"N": ..., ...}' [launches] [--generic]
+python tools/profile_one.py FAMILY '{"N": ..., ...}' [launches] [--generic] [--tf32x3] [--f32]
 """
 
 import json
@@ -20,11 +20,17 @@ def main():
     params = json.loads(sys.argv[2])
     launches = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 3
     generic = "--generic" in sys.argv
+    extra = _lib.FLAG_TF32X3 if "--tf32x3" in sys.argv else 0
+    temporal = [int(a.split("=")[1]) for a in sys.argv if a.startswith("--temporal=")]
+    if temporal:
+        extra |= _lib.FLAG_TEMPORAL
     kind = programs.original(fam)
     mv = machine_mod.live()
     sel = cases.select(kind, params, mv)
-    dtype = _lib.DTYPE_F32 if fam == "matmul" else _lib.DTYPE_I32
-    L = binding.make_launch(kind, params, sel.applied, dtype, generic=generic)
+    dtype = _lib.DTYPE_F32 if fam == "matmul" or "--f32" in sys.argv else _lib.DTYPE_I32
+    L = binding.make_launch(kind, params, sel.applied, dtype, generic=generic, extra_flags=extra)
+    if temporal:
+        L.tblock = temporal[0]
     shapes = programs.array_shapes(kind, params)
     bufs = []
     for a in programs.FAMILIES[fam].arrays:
