@@ -215,7 +215,7 @@ def main() -> int:
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-family extras")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-tune", action="store_true",
                     help="skip the tuners and use each grid's first entry (the recorded picks); "
                          "for profiler runs, whose timings are distorted")
