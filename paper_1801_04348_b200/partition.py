@@ -32,6 +32,7 @@ from dataclasses import dataclass
 from . import programs
 
 ROW_FAMILIES = ("transpose", "matvec", "matmul", "addition")
+SHARDED_FAMILIES = ("reverse",) + ROW_FAMILIES  # run_rows
 
 
 def _c_div(a: int, b: int) -> int:
@@ -232,6 +233,118 @@ def drive_local(gens):
         alive = nxt
 
 
+# ------------------------------------------------------- row-sharded runs --
+
+# operands every rank needs whole (matmul's b, mat-vec's x, the
+# transpose source); everything else is cut by the unit range
+REPLICATED = {"transpose": ("a",), "matvec": ("x",), "matmul": ("b",)}
+
+
+def share_range(family: str, P: dict, name: str, lo: int, hi: int) -> tuple[int, int]:
+    """(offset, count) in elements of the flat array ``name`` that units
+    [lo, hi) read or write -- the rule pk_run_host uses (array_range in
+    csrc/pk_abi.cu) to move only a rank's share."""
+    N = P["n"] if family == "matmul" else P["N"]
+    N = max(0, N)
+    total = {n: _numel(d) for n, d in programs.array_shapes(programs.original(family), P).items()}[name]
+    if name in REPLICATED.get(family, ()):
+        a, b = 0, total
+    elif family == "reverse":
+        a, b = (lo, hi) if name == "a" else (N - hi, N - lo)
+    elif family == "matvec" and name == "y":
+        a, b = lo, hi
+    elif family in ("transpose", "matvec", "matmul", "addition"):
+        a, b = lo * N, hi * N
+    else:
+        raise KeyError("%s is not a row-sharded family" % family)
+    a, b = max(0, a), min(total, b)
+    return a, max(0, b - a)
+
+
+def _numel(dims) -> int:
+    n = 1
+    for d in dims:
+        n *= max(0, d)
+    return n
+
+
+def run_rows(family: str, P: dict, arrays: dict, launch, *, group=None, root: int = 0) -> None:
+    """Run a row-sharded family over the ranks of ``group``, in place.
+
+    ``arrays``: name -> this rank's full-size flat tensor (the inputs are
+    read on ``root``).  ``launch(lo, hi)`` runs the selected leaf on units
+    [lo, hi) over those tensors (``pk_launch`` with lo/hi on the GPU).
+    Data movement is done once, outside the compute: the replicated operands
+    are broadcast from root, every other rank receives its share of the
+    sharded ones point-to-point, and the written shares (plus the uncovered
+    tail the program leaves untouched) are broadcast from their owners, so
+    every rank ends with the whole result.  The compute itself has no
+    collective.
+    """
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    fam = programs.FAMILIES[family]
+    names = [a.name for a in fam.arrays]
+    ranges = [split(family, P, r, world) for r in range(world)]
+    if world > 1:
+        for name in REPLICATED.get(family, ()):
+            dist.broadcast(arrays[name], src=root, group=group)
+        ops = []
+        for name in names:
+            if name in REPLICATED.get(family, ()):
+                continue
+            for r in range(world):
+                off, cnt = share_range(family, P, name, *ranges[r])
+                if r == root or cnt == 0:
+                    continue
+                view = arrays[name][off:off + cnt]
+                if rank == root:
+                    ops.append(dist.P2POp(dist.isend, view, r, group=group))
+                elif rank == r:
+                    ops.append(dist.P2POp(dist.irecv, view, root, group=group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+    lo, hi = ranges[rank]
+    if hi > lo:
+        launch(lo, hi)
+    if world > 1:
+        first, end, _ = units(family, P)
+        for name in fam.written:
+            for r in range(world):
+                off, cnt = share_range(family, P, name, *ranges[r])
+                if cnt:
+                    dist.broadcast(arrays[name][off:off + cnt], src=r, group=group)
+            # elements no rank covers keep their input values: root's
+            off, cnt = share_range(family, P, name, first, end)
+            total = arrays[name].numel()
+            for a, b in ((0, off), (off + cnt, total)):
+                if b > a:
+                    dist.broadcast(arrays[name][a:b], src=root, group=group)
+
+
+def pk_launcher(family: str, P: dict, arrays: dict, *, machine=None, dtype=None, stream=None):
+    """``launch(lo, hi)`` for run_rows on the GPU: the case selected at the
+    live device, bound to its kernel, launched over units [lo, hi) of the
+    caller's CUDA tensors (pk_launch with lo/hi)."""
+    import torch
+
+    from . import _lib, binding, cases
+
+    kind = programs.original(family)
+    sel = cases.select(kind, P, machine)
+    names = [a.name for a in programs.FAMILIES[family].arrays]
+    if dtype is None:
+        dtype = _lib.DTYPE_F32 if arrays[names[0]].dtype == torch.float32 else _lib.DTYPE_I32
+
+    def launch(lo, hi):
+        L = binding.make_launch(kind, P, sel.applied, dtype, lo=lo, hi=hi)
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _lib.launch(L, [arrays[n].data_ptr() for n in names], st)
+    return launch
+
+
 def unit_range_launch(family: str, P: dict, rank: int, world: int) -> tuple[int, int]:
     """lo/hi for pk_launch on rank's share (row / element families)."""
     lo, hi = split(family, P, rank, world)
@@ -243,4 +356,5 @@ def unit_range_launch(family: str, P: dict, rank: int, world: int) -> tuple[int,
 __all__ = [
     "units", "split", "halo_plan", "run_stencil", "drive", "drive_local", "TorchExchanger",
     "LocalExchanger", "Exchanger", "unit_range_launch", "ROW_FAMILIES", "programs",
+    "REPLICATED", "share_range", "run_rows", "pk_launcher", "SHARDED_FAMILIES",
 ]

@@ -173,3 +173,37 @@ def test_run_host_pipeline_matches_device_launch(cuda, family, params, share):
             # outside a share both sides keep the initial contents
             want = t.cpu().numpy().reshape(-1)
             assert np.array_equal(host[n].reshape(-1).view(np.int32), want.view(np.int32)), n
+
+
+@pytest.mark.parametrize("family,params", [
+    ("matmul", {"n": 512, "B0": 128, "ub1": 8, "s": 16}),
+    ("reverse", {"N": 1 << 16, "s": 16, "B": 256}),
+    ("matvec", {"N": 1024, "s": 1, "B": 256}),
+])
+def test_run_rows_with_pk_launcher(cuda, oracle_mod, family, params):
+    """run_rows' GPU launcher (pk_launch over the rank's unit range) in a
+    one-rank process group, against the oracle."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1801_04348_b200 import partition, programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    rng = np.random.default_rng(13)
+    init = {k: rng.integers(-40, 40, size=s).astype(np.int32) for k, s in shapes.items()}
+    want = oracle_mod.run(family, params, init)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=0, world_size=1)
+    try:
+        arrays = {k: torch.from_numpy(v.reshape(-1).copy()).cuda() for k, v in init.items()}
+        partition.run_rows(family, params, arrays, partition.pk_launcher(family, params, arrays))
+        torch.cuda.synchronize()
+        for name in programs.FAMILIES[family].written:
+            assert np.array_equal(arrays[name].cpu().numpy(), np.asarray(want[name]).reshape(-1)), name
+    finally:
+        dist.destroy_process_group()

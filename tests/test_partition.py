@@ -138,3 +138,93 @@ def test_gloo_world2_matches_oracle(tmp_path, oracle_mod, family, P):
     init = _initial(family, P)
     want = oracle_mod.run(family, P, {"a": init.reshape((-1,) if family == "jacobi" else (2 * P["N"], P["N"]))})["a"]
     assert np.array_equal(np.load(out), np.asarray(want).reshape(-1))
+
+
+# ---- row-sharded families: run_rows over gloo (broadcast / scatter / gather) ----
+
+ROW_CASES = [
+    ("reverse", {"N": 1000, "s": 4, "B": 16}),               # tail: N % (s*B) != 0
+    ("transpose", {"N": 40, "s": 2, "B0": 8, "B1": 4}),
+    ("matvec", {"N": 48, "s": 2, "B": 8}),
+    ("matmul", {"n": 40, "B0": 8, "ub1": 2, "s": 2}),        # row tail: 40 % 8 == 0, col tail 40 % 4 == 0
+    ("matmul", {"n": 36, "B0": 8, "ub1": 2, "s": 4}),        # uncovered rows 32..35 and columns
+    ("addition", {"N": 24, "B0": 4, "B1": 8}),
+]
+
+
+def _row_inputs(family, P, seed=5):
+    from paper_1801_04348_b200 import programs
+
+    shapes = programs.array_shapes(programs.original(family), P)
+    rng = np.random.default_rng(seed)
+    return {k: rng.integers(-50, 50, size=int(np.prod(s))).astype(np.int32) for k, s in shapes.items()}
+
+
+def oracle_launch(oracle_mod, family, P, arrays):
+    """CPU stand-in for pk_launch(lo, hi): the oracle's whole-program result,
+    copied back only over the written shares of [lo, hi)."""
+    from paper_1801_04348_b200 import programs
+
+    shapes = programs.array_shapes(programs.original(family), P)
+
+    def launch(lo, hi):
+        host = {k: v.numpy().reshape(shapes[k]) for k, v in arrays.items()}
+        res = oracle_mod.run(family, P, host)
+        for name in programs.FAMILIES[family].written:
+            off, cnt = partition.share_range(family, P, name, lo, hi)
+            full = np.asarray(res[name]).reshape(-1)
+            arrays[name][off:off + cnt] = torch.from_numpy(full[off:off + cnt].astype(np.int32))
+    return launch
+
+
+def _rows_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+
+    from oracle import oracle as oracle_mod
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    for i, (family, P) in enumerate(ROW_CASES):
+        init = _row_inputs(family, P)
+        # only root holds the real inputs; the others start from garbage
+        arrays = {k: torch.from_numpy(v.copy() if rank == 0 else np.full_like(v, 7777)) for k, v in init.items()}
+        partition.run_rows(family, P, arrays, oracle_launch(oracle_mod, family, P, arrays))
+        np.savez(out_path % (i, rank), **{k: v.numpy() for k, v in arrays.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_run_rows_gloo_every_rank_holds_the_oracle_result(tmp_path, oracle_mod, world):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1801_04348_b200 import programs
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "case%d_rank%d.npz")
+    mp.spawn(_rows_worker, args=(world, port, out), nprocs=world, join=True)
+    for i, (family, P) in enumerate(ROW_CASES):
+        init = _row_inputs(family, P)
+        shapes = programs.array_shapes(programs.original(family), P)
+        want = oracle_mod.run(family, P, {k: v.reshape(shapes[k]) for k, v in init.items()})
+        for r in range(world):
+            got = np.load(out % (i, r))
+            for name in programs.FAMILIES[family].written:
+                assert np.array_equal(got[name], np.asarray(want[name]).reshape(-1)), (family, P, r, name)
+            for name in partition.REPLICATED.get(family, ()):
+                assert np.array_equal(got[name], init[name]), (family, r, name)
+
+
+def test_share_range_rules():
+    P = {"n": 256, "B0": 64, "ub1": 8, "s": 16}
+    assert partition.share_range("matmul", P, "a", 64, 128) == (64 * 256, 64 * 256)
+    assert partition.share_range("matmul", P, "b", 64, 128) == (0, 256 * 256)
+    assert partition.share_range("reverse", {"N": 4096, "s": 4, "B": 64}, "c", 0, 1024) == (3072, 1024)
+    assert partition.share_range("matvec", {"N": 64, "s": 1, "B": 8}, "y", 8, 16) == (8, 8)
+    with pytest.raises(KeyError):
+        partition.share_range("jacobi", {"T": 1, "N": 10, "s": 1, "B": 2}, "a", 1, 2)
