@@ -127,10 +127,10 @@ __device__ __forceinline__ void j1_compute(const int *sb, bool al16, int *__rest
 // (the producer) fills window k mod S with one cp.async.bulk (the window
 // start rounded down to 16 bytes; the 8-byte remainder is the tile's shift)
 // as soon as the consumers have released it, and the other warps compute.
-// full[b] completes when window b has landed (TMA transaction count, or the
-// producer's arrive after a guarded fill); empty[b] when every consumer warp
-// has finished reading it.  No block-wide barrier: each consumer warp runs
-// ahead to the next landed window on its own.
+// full[b] completes when window b has landed (TMA transaction count) or, for
+// an edge window, when it is free for the consumers' own guarded fill;
+// empty[b] when every consumer warp has finished reading it.  No block-wide
+// barrier: each consumer warp runs ahead to the next landed window on its own.
 constexpr int kTmaPad = 16;    // words of slack per buffer for the alignment shift
 constexpr int kMaxStages = 8;  // ring depth limit (mbarrier header: 2 x 8 x 8 bytes)
 constexpr int kRingHeader = 2 * kMaxStages * 2;  // header size in ints
@@ -143,12 +143,19 @@ __device__ __forceinline__ void j1_issue(const int *src, int64_t xs, int tile, i
     tma_load_1d(buf, reinterpret_cast<const void *>(ga & ~(uintptr_t)15), bytes, bar);
 }
 
+// Barrier among the consumer warps only (named barrier 1; the producer warp
+// never joins it).
+__device__ __forceinline__ void consumers_sync(int nct) {
+    asm volatile("bar.sync 1, %0;" ::"r"((nct + 31) & ~31) : "memory");
+}
+
 // Producer warp.  Tiles [ta, tb) have their whole rounded window inside the
-// half and go by TMA; the one or two edge tiles outside it are filled by
-// guarded loads of the warp itself.
+// half and go by TMA; for the one or two edge tiles outside it the producer
+// only hands the (free) window to the consumers, which fill it with guarded
+// loads themselves (ordered by their named barrier).
 __device__ __forceinline__ void j1_produce(const int *__restrict__ src, int64_t x0, int tile, int64_t ntiles,
-                                           int64_t ta, int64_t tb, int64_t limit, int S, uint64_t *full,
-                                           uint64_t *empty, int *bufs) {
+                                           int64_t ta, int64_t tb, int S, uint64_t *full, uint64_t *empty,
+                                           int *bufs) {
     const int lane = threadIdx.x & 31;
     const int BW = tile + kTmaPad;
     uint32_t ephase = 0u;  // bit b: parity of empty[b]'s next completion
@@ -165,13 +172,8 @@ __device__ __forceinline__ void j1_produce(const int *__restrict__ src, int64_t 
                 fence_proxy_async();  // earlier generic accesses of buf before the async write
                 j1_issue(src, xs, tile, buf, &full[b]);
             }
-        } else {
-            for (int q = lane; q < tile + 8; q += 32) {
-                const int64_t i = xs - 4 + q;
-                buf[q] = (i >= 0 && i < limit) ? src[i] : 0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[b]);
+        } else if (lane == 0) {
+            mbar_arrive(&full[b]);
         }
         b = b + 1 == S ? 0 : b + 1;
     }
@@ -180,8 +182,8 @@ __device__ __forceinline__ void j1_produce(const int *__restrict__ src, int64_t 
 template <bool WIDE, bool FULL>
 __device__ __forceinline__ void j1_consume(const int *__restrict__ src, int *__restrict__ dst, int64_t lo,
                                            int64_t hi, int64_t x0, int tile, int64_t ntiles, int64_t ta,
-                                           int64_t tb, int S, uint64_t *full, uint64_t *empty, int *bufs,
-                                           int ctid, int nct) {
+                                           int64_t tb, int64_t limit, int S, uint64_t *full, uint64_t *empty,
+                                           int *bufs, int ctid, int nct) {
     const int BW = tile + kTmaPad;
     uint32_t fphase = 0u;  // bit b: parity of full[b]'s next completion
     int b = 0;
@@ -189,8 +191,18 @@ __device__ __forceinline__ void j1_consume(const int *__restrict__ src, int *__r
         mbar_wait(&full[b], (fphase >> b) & 1u);
         fphase ^= 1u << b;
         const int64_t xs = x0 + t * tile;
-        const int shift = (t >= ta && t < tb) ? (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2) : 0;
-        j1_compute<WIDE, FULL>(bufs + b * BW + shift, shift == 0, dst, lo, hi, xs, tile, true, ctid, nct);
+        int *buf = bufs + b * BW;
+        int shift = 0;
+        if (t >= ta && t < tb) {
+            shift = (int)((reinterpret_cast<uintptr_t>(src + xs - 4) & 15) >> 2);
+        } else {  // edge tile: guarded fill (block-uniform branch)
+            for (int q = ctid; q < tile + 8; q += nct) {
+                const int64_t i = xs - 4 + q;
+                buf[q] = (i >= 0 && i < limit) ? src[i] : 0;
+            }
+            consumers_sync(nct);
+        }
+        j1_compute<WIDE, FULL>(buf + shift, shift == 0, dst, lo, hi, xs, tile, true, ctid, nct);
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[b]);
         b = b + 1 == S ? 0 : b + 1;
@@ -218,15 +230,19 @@ __global__ void __launch_bounds__(288) k_jacobi1d_tma(const int *__restrict__ sr
     const int ctid = threadIdx.x - 32;
     const bool narrow = narrow_mode(mode, flag), full_warps = (nct & 31) == 0;
     if (threadIdx.x < 32)
-        j1_produce(src, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs);
+        j1_produce(src, x0, tile, ntiles, ta, tb, S, full, empty, bufs);
     else if (narrow && full_warps)
-        j1_consume<false, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+        j1_consume<false, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs, ctid,
+                                 nct);
     else if (narrow)
-        j1_consume<false, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+        j1_consume<false, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs, ctid,
+                                 nct);
     else if (full_warps)
-        j1_consume<true, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+        j1_consume<true, true>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs, ctid,
+                                 nct);
     else
-        j1_consume<true, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, S, full, empty, bufs, ctid, nct);
+        j1_consume<true, false>(src, dst, lo, hi, x0, tile, ntiles, ta, tb, limit, S, full, empty, bufs, ctid,
+                                 nct);
 }
 
 // window: positions [xs-4, xs+tile+4) at shared index pos - xs + 4 (tile % 4 == 0)
@@ -406,7 +422,8 @@ __device__ __forceinline__ void j2_compute(const int *base, int pitch, int s0, i
 // Warp-specialised TMA pipeline for 2-D tiles (same ring as the 1-D one):
 // the producer warp issues one bulk copy per window row (rows start on
 // 16-byte boundaries; the remainder is the row's shift) into window k mod S
-// once the consumer warps have released it.
+// once the consumer warps have released it; edge windows are filled by the
+// consumers.
 constexpr int kRowPad = 16;  // words of slack per window row for the alignment shift
 
 __device__ __forceinline__ uint32_t j2_row_bytes(int TJ, int sh) {
@@ -477,14 +494,8 @@ __device__ __forceinline__ void j2_produce(const int *__restrict__ src, int64_t 
         if (j2_window_ok(src, N, T.r0, T.nr, T.c0, TJ)) {
             fence_proxy_async();  // earlier generic accesses of buf before the async writes
             j2_issue(src, N, T.r0, T.nr, T.c0, TJ, buf, pitch, &full[b]);
-        } else {
-            for (int e = lane; e < (T.nr + 2) * pitch; e += 32) {
-                const int rr = e / pitch, cc = e - rr * pitch;
-                const int64_t col = T.c0 - 4 + cc;
-                buf[e] = (cc < TJ + 8 && col >= 0 && col < N) ? src[(T.r0 - 1 + rr) * N + col] : 0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[b]);
+        } else if (lane == 0) {
+            mbar_arrive(&full[b]);  // the consumers fill this edge window themselves
         }
         b = b + 1 == S ? 0 : b + 1;
     }
@@ -501,14 +512,23 @@ __device__ __forceinline__ void j2_consume(const int *__restrict__ src, int *__r
     int b = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const J2Tile T = j2_tile(t, ntc, rlo, rhi, TI, TJ);
+        const bool tma = j2_window_ok(src, N, T.r0, T.nr, T.c0, TJ);
         int s0 = 0, ds = 0;
-        if (j2_window_ok(src, N, T.r0, T.nr, T.c0, TJ)) {
+        if (tma) {
             s0 = (int)((reinterpret_cast<uintptr_t>(src + (T.r0 - 1) * N + T.c0 - 4) & 15) >> 2);
             ds = (int)(N & 3);
         }
         mbar_wait(&full[b], (fphase >> b) & 1u);
         fphase ^= 1u << b;
-        const int *buf = bufs + b * BW;
+        int *buf = bufs + b * BW;
+        if (!tma) {  // edge tile: guarded fill (block-uniform branch)
+            for (int e = ctid; e < (T.nr + 2) * pitch; e += nct) {
+                const int rr = e / pitch, cc = e - rr * pitch;
+                const int64_t col = T.c0 - 4 + cc;
+                buf[e] = (cc < TJ + 8 && col >= 0 && col < N) ? src[(T.r0 - 1 + rr) * N + col] : 0;
+            }
+            consumers_sync(nct);
+        }
         if (role.passes == 1)
             j2_march<WIDE, true>(role, buf, pitch, s0, ds, dst + T.r0 * N + T.c0, N, T.nr, T.c0, J, true);
         else
