@@ -303,4 +303,32 @@ int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     return fail(PK_E_UNSUPPORTED, "matmul: dtype %d", L.dtype);
 }
 
+// The reduction slice k in [k0, k1) of rows [lo, hi): c += a[:, k0:k1] b[k0:k1, :]
+// on the TMA-fed tile.  Slices run in ascending k on one stream give the bits
+// of a single launch -- between slices the fp32 accumulator simply lives in c
+// (every fma.rn rounds to fp32 either way).  pk_run_host uses it to start the
+// first row chunk while b is still crossing PCIe.
+bool matmul_kslice_ok(const pk_launch_t &L, int64_t slice) {
+    if (L.family != PK_FAMILY_MATMUL || L.dtype != PK_DTYPE_F32 || L.variant != PK_VARIANT_STAGED) return false;
+    if (L.flags & (PK_FLAG_GENERIC | PK_FLAG_TF32X3)) return false;
+    if (L.B0 <= 0 || L.ub1 <= 0 || L.s <= 0 || L.N <= 0 || slice <= 0 || slice % 128) return false;
+    const int64_t M = (L.N / L.B0) * L.B0, Nc = (L.N / (L.ub1 * L.s)) * L.ub1 * L.s;
+    int64_t rlo, rhi;
+    unit_range(L, 0, M, &rlo, &rhi);
+    return rhi > rlo && rlo % 4 == 0 && matmul_tma_fits(L.B0, L.ub1 * elems(L), rhi - rlo, Nc, slice, L.N);
+}
+
+int launch_matmul_kslice(const pk_launch_t &L, void *const *p, int64_t k0, int64_t k1, cudaStream_t st) {
+    if (!matmul_kslice_ok(L, k1 - k0) || k0 < 0 || k0 % 4 || k1 > (L.N / L.B0) * L.B0)
+        return fail(PK_E_UNSUPPORTED, "matmul: reduction slice [%lld, %lld) not provided for this leaf",
+                    (long long)k0, (long long)k1);
+    const int64_t M = (L.N / L.B0) * L.B0, Nc = (L.N / (L.ub1 * L.s)) * L.ub1 * L.s;
+    int64_t rlo, rhi;
+    unit_range(L, 0, M, &rlo, &rhi);
+    const float *a = static_cast<const float *>(p[0]), *b = static_cast<const float *>(p[1]);
+    float *c = static_cast<float *>(p[2]);
+    if (!aligned16(a) || !aligned16(b) || !aligned16(c)) return fail(PK_E_UNSUPPORTED, "matmul: unaligned operands");
+    return launch_matmul_tma(a + k0, b + k0 * L.N, c, L.N, rlo, rhi, Nc, k1 - k0, st);
+}
+
 }  // namespace pk

@@ -249,9 +249,11 @@ bool chunkable(const pk_launch_t &L) {
     }
 }
 
+constexpr int kSlices = 4;  // reduction slices of matmul's first row chunk
+
 struct HostRun {
     cudaStream_t h2d = nullptr, d2h = nullptr, cs[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2 * kMaxChunks] = {};
+    cudaEvent_t ev[2 * kMaxChunks + kSlices] = {};
     void *dev[3] = {nullptr, nullptr, nullptr};
 };
 
@@ -294,7 +296,8 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.d2h, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[0], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[1], cudaStreamNonBlocking);
-    for (int k = 0; k < 2 * nchunks && e == cudaSuccess; k++) e = cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming);
+    for (int k = 0; k < 2 * nchunks + kSlices && e == cudaSuccess; k++)
+        e = cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) rc = fail(PK_E_CUDA, "stream/event setup: %s", cudaGetErrorString(e));
 
     auto chunk = [&](int k) {
@@ -317,9 +320,18 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         array_range(chunk(0), i, spec.elems[i], &off, &cnt);
         whole[i] = nchunks == 1 || (off == 0 && cnt == spec.elems[i]);
     }
-    auto up = [&](const pk_launch_t &C, int i) -> int {
-        int64_t off, cnt;
-        array_range(C, i, spec.elems[i], &off, &cnt);
+    // Matmul: the first row chunk runs reduction slice by reduction slice as
+    // b's rows arrive (launch_matmul_kslice -- the bits of one launch), so the
+    // kernels start before the 256 MiB of b have crossed PCIe.
+    int64_t slice = 0, Kred = 0;
+    if (rc == PK_OK && nchunks > 1 && L->family == PK_FAMILY_MATMUL && L->B0 > 0) {
+        Kred = (N / L->B0) * L->B0;
+        slice = Kred / kSlices / 128 * 128;
+        if (slice <= 0 || !matmul_kslice_ok(chunk(0), slice) ||
+            !matmul_kslice_ok(chunk(0), Kred - (kSlices - 1) * slice))
+            slice = 0;
+    }
+    auto up_range = [&](int i, int64_t off, int64_t cnt) -> int {
         char *d = static_cast<char *>(R.dev[i]) + off * 4;
         if (cnt && host_ptrs[i]) {
             cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * 4, (size_t)cnt * 4,
@@ -329,6 +341,11 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
             cudaMemsetAsync(d, 0, (size_t)cnt * 4, R.h2d);  // missing arrays are zero-filled (interp.py:79-81)
         }
         return PK_OK;
+    };
+    auto up = [&](const pk_launch_t &C, int i) -> int {
+        int64_t off, cnt;
+        array_range(C, i, spec.elems[i], &off, &cnt);
+        return up_range(i, off, cnt);
     };
     auto down = [&](const pk_launch_t &C, int i) -> int {
         int64_t off, cnt;
@@ -340,7 +357,7 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         return x == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(x));
     };
     for (int i = 0; i < spec.count && rc == PK_OK; i++)
-        if (whole[i]) rc = up(nchunks == 1 ? *L : chunk(0), i);
+        if (whole[i] && !(slice && i == 1)) rc = up(nchunks == 1 ? *L : chunk(0), i);
     for (int k = 0; k < nchunks && rc == PK_OK; k++) {
         const pk_launch_t C = chunk(k);
         for (int i = 0; i < spec.count && rc == PK_OK; i++)
@@ -349,7 +366,19 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         cudaEventRecord(R.ev[2 * k], R.h2d);
         cudaStream_t cs = R.cs[k & 1];
         cudaStreamWaitEvent(cs, R.ev[2 * k], 0);
-        rc = dispatch(C, R.dev, cs);
+        if (k == 0 && slice) {
+            for (int j = 0; j < kSlices && rc == PK_OK; j++) {  // b's rows (k) slice by slice
+                const int64_t r0 = j * slice, r1 = j + 1 < kSlices ? (j + 1) * slice : N;
+                rc = up_range(1, r0 * N, (r1 - r0) * N);
+                cudaEventRecord(R.ev[2 * nchunks + j], R.h2d);
+            }
+            for (int j = 0; j < kSlices && rc == PK_OK; j++) {
+                cudaStreamWaitEvent(cs, R.ev[2 * nchunks + j], 0);
+                rc = launch_matmul_kslice(C, R.dev, j * slice, j + 1 < kSlices ? (j + 1) * slice : Kred, cs);
+            }
+        } else {
+            rc = dispatch(C, R.dev, cs);
+        }
         if (rc) break;
         cudaEventRecord(R.ev[2 * k + 1], cs);
         cudaStreamWaitEvent(R.d2h, R.ev[2 * k + 1], 0);
@@ -370,8 +399,8 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     for (int i = 0; i < spec.count; i++)
         if (R.dev[i]) cudaFreeAsync(R.dev[i], R.d2h);
     if (R.d2h) cudaStreamSynchronize(R.d2h);
-    for (int k = 0; k < 2 * kMaxChunks; k++)
-        if (R.ev[k]) cudaEventDestroy(R.ev[k]);
+    for (cudaEvent_t ev : R.ev)
+        if (ev) cudaEventDestroy(ev);
     for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h})
         if (s) cudaStreamDestroy(s);
     return rc;
