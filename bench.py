@@ -456,8 +456,8 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
             out[fam]["traffic"] = {"dram_bytes": rec["bytes"], "algorithmic_bytes": per,
                                    "ratio": round(rec["bytes"] / per, 4), "kernel": rec["kernel"],
                                    "source": rec["report"]}
-        if fam == "jacobi":  # temporally blocked variant, reported separately (same results)
-            for h in (7, 15):
+        if fam in ("jacobi", "jacobi2d"):  # temporally blocked variant, reported separately (same results)
+            for h in ((7, 15) if fam == "jacobi" else (3, 7)):
                 Lt = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32,
                                          extra_flags=_lib.FLAG_TEMPORAL)
                 Lt.tblock = h
@@ -469,7 +469,7 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
                 torch.cuda.synchronize()
                 tms = e0.elapsed_time(e1)
                 tg = work / (tms * 1e-3) / 1e9
-                out["jacobi_temporal_h%d" % h] = {
+                out["%s_temporal_h%d" % (fam, h)] = {
                     "params": run_params, "ms": round(tms, 3), "value": round(tg, 1), "unit": unit,
                     "speedup_vs_per_step": round(ms / tms, 2),
                     "note": "algorithmic bytes of the per-step program / time: exceeds the HBM roofline "

@@ -932,10 +932,26 @@ int launch_jacobi2d(const pk_launch_t &L, void *const *p, cudaStream_t st) {
         rc = range_flag(a, 2 * L.N * L.N, kBound5, &flag, st);
         if (rc) return rc;
     }
-    for (int64_t t = 0; t < L.T && rc == PK_OK; t++) {
+    const bool temporal = (L.flags & PK_FLAG_TEMPORAL) && L.hi <= 0;  // whole-program runs only
+    int hmax = L.tblock > 0 ? (int)L.tblock : 7;
+    if (hmax > 11) hmax = 11;
+    if (hmax % 2 == 0) hmax -= 1;  // odd: a pass never writes the half it reads
+    for (int64_t t = 0; t < L.T && rc == PK_OK;) {
+        // temporal passes leave the last step to an ordinary sweep (k_jacobi2d_temporal.cu)
+        int h = 1;
+        if (temporal && L.T - t > 2) {
+            h = (int)((L.T - t - 1) < hmax ? (L.T - t - 1) : hmax);
+            if (h % 2 == 0) h -= 1;
+        }
+        if (h > 1) {
+            rc = jacobi2d_temporal_pass(L, a, lo, hi, e.I, e.J, t, h, flag, sweep_mode(L, flag), st);
+            t += h;
+            continue;
+        }
         const bool even = (t % 2) == 0;
         // t even reads half 0 and writes half 1 (a[N+i][j] = ...), t odd the reverse
         rc = sweep2d_impl(L, even ? a : half1, even ? half1 : a, lo, hi, flag, st);
+        t++;
     }
     if (flag) cudaFreeAsync(flag, st);
     return rc;

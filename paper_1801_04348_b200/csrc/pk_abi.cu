@@ -154,8 +154,8 @@ int validate(const pk_launch_t *L, int nptrs) {
         return fail(PK_E_UNSUPPORTED, "dtype %d not provided for family %d", L->dtype, L->family);
     if ((L->flags & PK_FLAG_TF32X3) && !(L->family == PK_FAMILY_MATMUL && L->dtype == PK_DTYPE_F32))
         return fail(PK_E_UNSUPPORTED, "3xTF32 applies to float32 matmul only");
-    if ((L->flags & PK_FLAG_TEMPORAL) && L->family != PK_FAMILY_JACOBI1D)
-        return fail(PK_E_UNSUPPORTED, "temporal blocking is provided for the 1-D Jacobi program only");
+    if ((L->flags & PK_FLAG_TEMPORAL) && L->family != PK_FAMILY_JACOBI1D && L->family != PK_FAMILY_JACOBI2D)
+        return fail(PK_E_UNSUPPORTED, "temporal blocking is provided for the Jacobi programs only");
     return PK_OK;
 }
 

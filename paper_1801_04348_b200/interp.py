@@ -178,7 +178,7 @@ def run_program(
     force the program's literal thread mapping instead of the tuned tile.
     Optional variants, reported separately from the leaves: ``tf32x3``
     (float32 matmul on tcgen05, fp32-level accuracy) and ``temporal=h``
-    (1-D Jacobi advancing h steps per HBM pass, bit-identical).
+    (1-D / 2-D Jacobi advancing h steps per HBM pass, bit-identical).
     """
     global _last
     if tracer is not None:
@@ -246,7 +246,7 @@ def run_program(
     L = binding.make_launch(kind, P, applied, dtype, generic=generic,
                             extra_flags=(_lib.FLAG_TF32X3 if tf32x3 else 0) | (_lib.FLAG_TEMPORAL if temporal else 0))
     if temporal:
-        L.tblock = int(temporal)  # steps fused per HBM pass (odd; 1-D Jacobi only)
+        L.tblock = int(temporal)  # steps fused per HBM pass (odd; Jacobi programs only)
     stream = torch.cuda.current_stream(dev).cuda_stream
 
     with torch.cuda.device(dev):

@@ -50,3 +50,31 @@ def test_occupancy_model_on_live_device(cuda, oracle_mod):
     assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
     info = interp.last_run()
     assert info.case == 1 and not info.fallback
+
+
+@pytest.mark.parametrize("h", [3, 5, 11])
+@pytest.mark.parametrize("T", [0, 1, 2, 3, 4, 6, 9, 14])
+def test_temporal_jacobi2d_matches_oracle(cuda, oracle_mod, h, T):
+    """2-D temporal blocking: bit-identical to the per-step program, including
+    uncovered tails (J < N-2, I < N-2), odd N and tiles cut by the edges."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(T * 17 + h)
+    for N, s, B0, B1 in ((258, 4, 8, 8), (301, 2, 4, 16), (130, 1, 16, 4)):
+        params = {"T": T, "N": N, "s": s, "B0": B0, "B1": B1}
+        a = rng.integers(-(1 << 20), 1 << 20, size=(2 * N, N)).astype(np.int32)
+        want = oracle_mod.run("jacobi2d", params, {"a": a})["a"]
+        got = run_program(programs.source("jacobi2d"), params, {"a": a}, temporal=h)["a"]
+        assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1)), (T, h, N)
+
+
+def test_temporal_jacobi2d_wide_values(cuda, oracle_mod):
+    """Full-range int32 inputs force 64-bit sums inside the fused steps."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(21)
+    params = {"T": 11, "N": 386, "s": 4, "B0": 8, "B1": 16}
+    a = rng.integers(-(2**31), 2**31 - 1, size=(2 * 386, 386)).astype(np.int32)
+    want = oracle_mod.run("jacobi2d", params, {"a": a})["a"]
+    got = run_program(programs.source("jacobi2d"), params, {"a": a}, temporal=5)["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
