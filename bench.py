@@ -536,7 +536,7 @@ TUNE_GRIDS = {
     "transpose": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((64, 8, 8), (32, 8, 4), (64, 16, 4),
                                                                  (32, 32, 1), (128, 8, 4))],
     "jacobi": [{"B": b, "s": s} for b, s in ((256, 16), (256, 8), (128, 32), (512, 8), (1024, 4))],
-    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((8, 32, 16), (32, 8, 32), (64, 4, 32),
+    "jacobi2d": [{"B0": b0, "B1": b1, "s": s} for b0, b1, s in ((64, 4, 32), (8, 32, 16), (32, 8, 32),
                                                                 (32, 8, 16), (16, 16, 32))],
     "matvec": [{"B": b, "s": s} for b, s in ((256, 1), (128, 1), (64, 2), (512, 1), (32, 4))],
 }
