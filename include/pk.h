@@ -143,6 +143,22 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
 int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
                     void *stream);
 
+/* One program over several GPUs of this process (single-process multi-GPU,
+ * the partitioner of SURVEY 8(e) in native code).  Device k
+ * (devices[k], which may repeat) holds full-size arrays with the program's
+ * global indexing -- dev_ptrs[k * nptrs + i] is array i on device k -- with
+ * the inputs present on every device, and computes its aligned share of the
+ * units (rows; elements for reversal; interior positions / rows for the
+ * stencils).  The row families need no exchange.  The stencils refresh
+ * ghost zones of width `halo` (<= 0: 16; capped by the smallest slab and T)
+ * every `halo` steps with peer copies (cudaMemcpyPeerAsync: NVLink between
+ * B200s), recomputing the overlap in between.  With gather != 0 every
+ * device's written share (both Jacobi halves) is copied into devices[0]'s
+ * arrays, which then hold the whole result, bit-identical to pk_launch.
+ * L->lo / L->hi must be 0.  Synchronises every device. */
+int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *const *dev_ptrs, int nptrs,
+                    int64_t halo, int gather);
+
 /* Value-range check for the Jacobi fast path: *narrow = 1 when every value
  * of the double buffer `a` is within the PK_FLAG_NARROW bound (a Jacobi
  * average never leaves the range of its inputs, so the bound then holds for

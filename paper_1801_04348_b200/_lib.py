@@ -53,6 +53,7 @@ EXPORTS = (
     "pk_query_machine",
     "pk_launch",
     "pk_run_host",
+    "pk_launch_multi",
     "pk_jacobi_sweep",
     "pk_jacobi_narrow",
     "pk_footprint_words",
@@ -140,6 +141,9 @@ def load() -> ctypes.CDLL:
         lib.pk_launch.restype = ctypes.c_int
         lib.pk_run_host.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int]
         lib.pk_run_host.restype = ctypes.c_int
+        lib.pk_launch_multi.argtypes = [ctypes.POINTER(PkLaunch), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int64, ctypes.c_int]
+        lib.pk_launch_multi.restype = ctypes.c_int
         lib.pk_jacobi_sweep.argtypes = [ctypes.POINTER(PkLaunch), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
         lib.pk_jacobi_sweep.restype = ctypes.c_int
         lib.pk_jacobi_narrow.argtypes = [ctypes.POINTER(PkLaunch), vp, ctypes.POINTER(ctypes.c_int32), vp]
@@ -205,6 +209,16 @@ def run_host(L: PkLaunch, host_ptrs, device: int = 0) -> None:
     lib = load()
     arr = ptr_array(host_ptrs)
     check(lib.pk_run_host(ctypes.byref(L), arr, len(host_ptrs), device))
+
+
+def launch_multi(L: PkLaunch, devices, ptr_lists, halo: int = 0, gather: bool = True) -> None:
+    """pk_launch_multi: ptr_lists[k] are the arrays (declaration order) on devices[k]."""
+    lib = load()
+    n = len(devices)
+    devs = (ctypes.c_int * n)(*devices)
+    flat = ptr_array([p for ptrs in ptr_lists for p in ptrs])
+    nptrs = len(ptr_lists[0]) if ptr_lists else 0
+    check(lib.pk_launch_multi(ctypes.byref(L), n, devs, flat, nptrs, int(halo), 1 if gather else 0))
 
 
 def jacobi_sweep(L: PkLaunch, src: int, dst: int, lo: int, hi: int, stream: int = 0) -> None:

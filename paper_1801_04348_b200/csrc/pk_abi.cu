@@ -233,6 +233,7 @@ int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void 
 namespace {
 
 constexpr int kMaxChunks = 8;                  // pipeline depth limit of pk_run_host
+constexpr int kMaxDevices = 64;                // pk_launch_multi
 constexpr int64_t kChunkBytes = 48ll << 20;    // PCIe bytes per chunk (~1 ms of transfer)
 
 // Units (rows, or elements for reversal) a host-buffer run may be cut into:
@@ -404,6 +405,224 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h})
         if (s) cudaStreamDestroy(s);
     return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Single-process multi-GPU.
+
+namespace {
+
+// Covered units of a launch and the partitioner's alignment (one leaf tile),
+// as the family launchers compute them; false when there is nothing to split.
+bool covered_units(const pk_launch_t &L, int64_t *u0, int64_t *u1, int64_t *align) {
+    const int64_t N = L.N, E = elems(L);
+    auto cover = [](int64_t n, int64_t t) { return t > 0 && n > 0 ? (n / t) * t : (int64_t)0; };
+    *u0 = 0;
+    switch (L.family) {
+        case PK_FAMILY_REVERSE: *u1 = cover(N, L.s * L.B); *align = 4 * L.s * L.B; break;
+        case PK_FAMILY_TRANSPOSE: *u1 = cover(N, L.B0); *align = L.B0 > 4 ? L.B0 : 4; break;
+        case PK_FAMILY_MATVEC: *u1 = cover(N, L.s * L.B); *align = L.s * L.B; break;
+        case PK_FAMILY_MATMUL: *u1 = cover(N, L.B0); *align = L.B0 > 4 ? L.B0 : 4; break;
+        case PK_FAMILY_ADDITION: *u1 = cover(N, L.B0); *align = L.B0; break;
+        case PK_FAMILY_JACOBI1D: *u0 = 1; *u1 = 1 + cover(N - 2, L.s * L.B); *align = L.s * L.B; break;
+        case PK_FAMILY_JACOBI2D: *u0 = 1; *u1 = 1 + cover(N - 2, L.B0); *align = L.B0; break;
+        default: return false;
+    }
+    (void)E;
+    return L.s >= 0 && L.B >= 0 && L.B0 >= 0 && L.B1 >= 0 && L.ub1 >= 0 && *align > 0 && *u1 > *u0;
+}
+
+// Device k's share: whole tiles where there are enough (partition.split).
+void share(int64_t u0, int64_t u1, int64_t align, int k, int n, int64_t *lo, int64_t *hi) {
+    const int64_t total = u1 - u0, blocks = total / align;
+    if (n <= 1) {
+        *lo = u0;
+        *hi = u1;
+    } else if (blocks >= n) {
+        *lo = u0 + blocks * k / n * align;
+        *hi = k == n - 1 ? u1 : u0 + blocks * (k + 1) / n * align;
+    } else {
+        *lo = u0 + total * k / n;
+        *hi = u0 + total * (k + 1) / n;
+    }
+}
+
+struct Multi {
+    int n = 0;
+    const int *dev = nullptr;
+    cudaStream_t st[kMaxDevices] = {};
+    cudaEvent_t done[kMaxDevices] = {}, copied[kMaxDevices] = {};
+    ~Multi() {
+        for (int k = 0; k < n; k++) {
+            cudaSetDevice(dev[k]);
+            if (st[k]) cudaStreamDestroy(st[k]);
+            if (done[k]) cudaEventDestroy(done[k]);
+            if (copied[k]) cudaEventDestroy(copied[k]);
+        }
+    }
+};
+
+int peer_copy(void *dst, int ddev, const void *src, int sdev, size_t bytes, cudaStream_t st) {
+    if (!bytes) return PK_OK;
+    cudaError_t e = cudaMemcpyPeerAsync(dst, ddev, src, sdev, bytes, st);
+    return e == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "peer copy %d -> %d: %s", sdev, ddev, cudaGetErrorString(e));
+}
+
+}  // namespace
+
+int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *const *dev_ptrs, int nptrs,
+                    int64_t halo, int gather) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    if (ndev < 1 || ndev > kMaxDevices || !devices || !dev_ptrs)
+        return fail(PK_E_PARAM, "pk_launch_multi: %d devices (1..%d) with their arrays", ndev, kMaxDevices);
+    if (L->hi > 0) return fail(PK_E_PARAM, "pk_launch_multi splits the units itself: leave lo/hi at 0");
+    for (int i = 0; i < ndev * nptrs; i++)
+        if (!dev_ptrs[i]) return fail(PK_E_PARAM, "array %d of device %d is a null pointer", i % nptrs, i / nptrs);
+    auto ptrs = [&](int k) { return dev_ptrs + (size_t)k * nptrs; };
+
+    Multi M;
+    M.n = ndev;
+    M.dev = devices;
+    for (int k = 0; k < ndev; k++) {
+        cudaError_t e = cudaSetDevice(devices[k]);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&M.st[k], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&M.done[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&M.copied[k], cudaEventDisableTiming);
+        if (e != cudaSuccess) return fail(PK_E_CUDA, "device %d setup: %s", devices[k], cudaGetErrorString(e));
+    }
+    auto finish = [&](int code) {
+        for (int k = 0; k < ndev; k++) {
+            cudaSetDevice(devices[k]);
+            cudaError_t e = cudaStreamSynchronize(M.st[k]);
+            if (e != cudaSuccess && code == PK_OK) code = fail(PK_E_CUDA, "device %d: %s", devices[k], cudaGetErrorString(e));
+        }
+        return code;
+    };
+
+    int64_t u0, u1, align;
+    const bool stencil = L->family == PK_FAMILY_JACOBI1D || L->family == PK_FAMILY_JACOBI2D;
+    if (ndev == 1 || !covered_units(*L, &u0, &u1, &align)) {  // nothing to split: device 0 runs it
+        cudaSetDevice(devices[0]);
+        return finish(dispatch(*L, ptrs(0), M.st[0]));
+    }
+
+    if (!stencil) {
+        // row / element shares, no exchange; then the written shares to device 0
+        pk_launch_t Ls[kMaxDevices];
+        for (int k = 0; k < ndev && rc == PK_OK; k++) {
+            Ls[k] = *L;
+            share(u0, u1, align, k, ndev, &Ls[k].lo, &Ls[k].hi);
+            if (Ls[k].hi <= Ls[k].lo) continue;
+            cudaSetDevice(devices[k]);
+            rc = dispatch(Ls[k], ptrs(k), M.st[k]);
+            cudaEventRecord(M.done[k], M.st[k]);
+        }
+        if (rc || !gather) return finish(rc);
+        ArraySpec spec;
+        array_spec(*L, &spec);
+        cudaSetDevice(devices[0]);
+        for (int k = 1; k < ndev && rc == PK_OK; k++) {
+            if (Ls[k].hi <= Ls[k].lo) continue;
+            cudaStreamWaitEvent(M.st[0], M.done[k], 0);
+            for (int i = 0; i < spec.count && rc == PK_OK; i++) {
+                if (!spec.written[i]) continue;
+                int64_t off, cnt;
+                array_range(Ls[k], i, spec.elems[i], &off, &cnt);
+                rc = peer_copy(static_cast<char *>(ptrs(0)[i]) + off * 4, devices[0],
+                               static_cast<const char *>(ptrs(k)[i]) + off * 4, devices[k], (size_t)cnt * 4, M.st[0]);
+            }
+        }
+        return finish(rc);
+    }
+
+    // ---- stencils: slabs with ghost zones of width h refreshed every h steps
+    pk_launch_t Ln = *L;
+    if (!(Ln.flags & PK_FLAG_NARROW)) {  // the range check once (inputs are replicated)
+        int narrow = 0;
+        cudaSetDevice(devices[0]);
+        rc = jacobi_narrow(Ln, ptrs(0)[0], &narrow, M.st[0]);
+        if (rc) return finish(rc);
+        if (narrow) Ln.flags |= PK_FLAG_NARROW;
+    }
+    const bool one = L->family == PK_FAMILY_JACOBI1D;
+    const int64_t N = L->N, row = one ? 1 : N, half = one ? N : N * N;
+    int64_t lo[kMaxDevices], hi[kMaxDevices], min_slab = u1 - u0;
+    for (int k = 0; k < ndev; k++) {
+        share(u0, u1, align, k, ndev, &lo[k], &hi[k]);
+        if (hi[k] - lo[k] < min_slab) min_slab = hi[k] - lo[k];
+    }
+    int64_t h = halo > 0 ? halo : 16;
+    if (h > min_slab) h = min_slab;
+    if (h > L->T) h = L->T;
+    if (h < 1) h = 1;
+    // step t reads s(t), writes d(t): 1-D t even reads the upper half, 2-D the lower
+    auto src_half = [&](int k, int64_t t) -> int * {
+        int *a = static_cast<int *>(ptrs(k)[0]);
+        const bool upper = one ? (t % 2 == 0) : (t % 2 == 1);
+        return upper ? a + half : a;
+    };
+    for (int64_t t = 0; t < L->T && rc == PK_OK;) {
+        const int64_t hb = (L->T - t) < h ? (L->T - t) : h;
+        // exchange: the ghost rows of s(t) on both sides of every boundary; the
+        // source device waits before overwriting them (step t+1 writes s(t))
+        if (min_slab > 0) {
+            for (int k = 0; k < ndev; k++) {
+                cudaSetDevice(devices[k]);
+                cudaEventRecord(M.done[k], M.st[k]);
+            }
+            for (int k = 0; k < ndev && rc == PK_OK; k++) {
+                cudaSetDevice(devices[k]);
+                if (k > 0) {  // rows [lo_k - hb, lo_k) from device k-1
+                    cudaStreamWaitEvent(M.st[k], M.done[k - 1], 0);
+                    rc = peer_copy(src_half(k, t) + (lo[k] - hb) * row, devices[k],
+                                   src_half(k - 1, t) + (lo[k] - hb) * row, devices[k - 1],
+                                   (size_t)(hb * row) * 4, M.st[k]);
+                }
+                if (rc == PK_OK && k + 1 < ndev) {  // rows [hi_k, hi_k + hb) from device k+1
+                    cudaStreamWaitEvent(M.st[k], M.done[k + 1], 0);
+                    rc = peer_copy(src_half(k, t) + hi[k] * row, devices[k], src_half(k + 1, t) + hi[k] * row,
+                                   devices[k + 1], (size_t)(hb * row) * 4, M.st[k]);
+                }
+                cudaEventRecord(M.copied[k], M.st[k]);
+            }
+            for (int k = 0; k < ndev; k++) {
+                cudaSetDevice(devices[k]);
+                if (k > 0) cudaStreamWaitEvent(M.st[k], M.copied[k - 1], 0);
+                if (k + 1 < ndev) cudaStreamWaitEvent(M.st[k], M.copied[k + 1], 0);
+            }
+        }
+        for (int k = 0; k < ndev && rc == PK_OK; k++) {
+            cudaSetDevice(devices[k]);
+            for (int64_t j = 0; j < hb && rc == PK_OK; j++) {
+                const int64_t ext = hb - 1 - j;  // overlap still valid after this step
+                const int64_t a = lo[k] - ext > u0 ? lo[k] - ext : u0;
+                const int64_t b = hi[k] + ext < u1 ? hi[k] + ext : u1;
+                int *src = src_half(k, t + j);
+                int *base = static_cast<int *>(ptrs(k)[0]);
+                int *dst = src == base ? base + half : base;
+                rc = one ? sweep_jacobi1d(Ln, src, dst, a, b, M.st[k]) : sweep_jacobi2d(Ln, src, dst, a, b, M.st[k]);
+            }
+        }
+        t += hb;
+    }
+    if (rc == PK_OK && gather) {  // both halves of every slab to device 0
+        for (int k = 0; k < ndev; k++) {
+            cudaSetDevice(devices[k]);
+            cudaEventRecord(M.done[k], M.st[k]);
+        }
+        cudaSetDevice(devices[0]);
+        for (int k = 1; k < ndev && rc == PK_OK; k++) {
+            cudaStreamWaitEvent(M.st[0], M.done[k], 0);
+            for (int hsel = 0; hsel < 2 && rc == PK_OK; hsel++) {
+                const int64_t off = hsel * half + lo[k] * row;
+                rc = peer_copy(static_cast<int *>(ptrs(0)[0]) + off, devices[0],
+                               static_cast<const int *>(ptrs(k)[0]) + off, devices[k],
+                               (size_t)((hi[k] - lo[k]) * row) * 4, M.st[0]);
+            }
+        }
+    }
+    return finish(rc);
 }
 
 }  // extern "C"

@@ -170,6 +170,8 @@ def run_program(
     case: int | None = None,
     tf32x3: bool = False,
     temporal: int = 0,
+    devices=None,
+    halo: int = 0,
 ) -> dict:
     """Execute the whole program on the GPU; returns the final array contents.
 
@@ -179,6 +181,9 @@ def run_program(
     Optional variants, reported separately from the leaves: ``tf32x3``
     (float32 matmul on tcgen05, fp32-level accuracy) and ``temporal=h``
     (1-D / 2-D Jacobi advancing h steps per HBM pass, bit-identical).
+    ``devices=[d0, d1, ...]``: run on several GPUs of this process
+    (pk_launch_multi: unit shares, ghost-zone exchange of width ``halo``
+    by peer copies for the stencils); the result is gathered on ``d0``.
     """
     global _last
     if tracer is not None:
@@ -203,6 +208,11 @@ def run_program(
     torch = _torch()
     if not torch.cuda.is_available():
         raise RuntimeError("run_program needs a CUDA device (sm_100a); there is no CPU fallback")
+    if devices is not None:
+        devices = [int(d) for d in devices]
+        if not devices:
+            raise ValueError("devices must name at least one GPU")
+        device = devices[0]
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     mv = None
     if machine is None or machine == "live":
@@ -269,7 +279,14 @@ def run_program(
             owned[a.name] = t
             bufs.append(t)
         if all(_numel(shapes[a.name]) > 0 for a in fam.arrays):
-            _lib.launch(L, [b.data_ptr() for b in bufs], stream)
+            if devices is not None and len(devices) > 1:
+                # inputs replicated on every device (full-size arrays, global indexing)
+                reps = [bufs] + [[b.to(torch.device("cuda", d), copy=True) for b in bufs] for d in devices[1:]]
+                for d in set(devices):
+                    torch.cuda.synchronize(d)
+                _lib.launch_multi(L, devices, [[b.data_ptr() for b in r] for r in reps], halo=halo)
+            else:
+                _lib.launch(L, [b.data_ptr() for b in bufs], stream)
         torch.cuda.current_stream(dev).synchronize()
 
     _last = RunInfo(kind.family, case_index, tuple(applied), fallback, binding.describe(L),
