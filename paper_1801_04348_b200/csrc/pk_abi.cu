@@ -462,6 +462,28 @@ struct Multi {
     }
 };
 
+// Direct peer access between every pair of distinct devices that support it
+// (NVLink DMA for the peer copies), enabled once per pair for the process.
+void enable_peers(int ndev, const int *devices) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < ndev; i++)
+        for (int j = 0; j < ndev; j++) {
+            const int a = devices[i], b = devices[j];
+            if (a == b) continue;
+            bool seen = false;
+            for (const auto &p : done) seen |= p.first == a && p.second == b;
+            if (seen) continue;
+            done.emplace_back(a, b);
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) == cudaSuccess && can) {
+                cudaSetDevice(a);
+                if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+            }
+        }
+}
+
 int peer_copy(void *dst, int ddev, const void *src, int sdev, size_t bytes, cudaStream_t st) {
     if (!bytes) return PK_OK;
     cudaError_t e = cudaMemcpyPeerAsync(dst, ddev, src, sdev, bytes, st);
@@ -481,6 +503,7 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         if (!dev_ptrs[i]) return fail(PK_E_PARAM, "array %d of device %d is a null pointer", i % nptrs, i / nptrs);
     auto ptrs = [&](int k) { return dev_ptrs + (size_t)k * nptrs; };
 
+    enable_peers(ndev, devices);
     Multi M;
     M.n = ndev;
     M.dev = devices;
