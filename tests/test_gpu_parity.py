@@ -234,3 +234,92 @@ def test_matmul_tf32x3_tcgen05_within_tolerance(cuda, oracle_mod):
         scale = (np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64))).max()
         err = np.abs(got.astype(np.float64) - want).max() / scale
         assert err <= _matmul_tol(n), (n, err)
+
+
+# ---- BASELINE-size parity through properties that do not need the CPU oracle ----
+
+
+def test_matmul_full_size_integer_valued_exact(cuda):
+    """n = 8192 (BASELINE configs[1]) on the tuned TMA tile: integer-valued fp32
+    in [-8, 8] keeps every partial sum an integer below 2^24, so the result
+    must equal an exact binary64 product (torch float64 on the GPU)."""
+    torch = cuda
+    from paper_1801_04348_b200 import last_run, programs
+
+    n = 8192
+    g = torch.Generator(device="cuda").manual_seed(17)
+    a = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    b = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    c = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    got = _run(programs.source("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": 16}, {"a": a, "b": b, "c": c})["c"]
+    assert last_run().applied == ()
+    want = c.double() + a.double() @ b.double()
+    assert torch.equal(got.reshape(n, n).double(), want)
+
+
+def _jacobi1d_torch(a, N, T, P):
+    """Restatement of jacobi.mfk on the GPU (int64 sums, truncating division)."""
+    torch = __import__("torch")
+    h = [a[:N].long(), a[N:2 * N].long()]
+    for t in range(T):
+        src, dst = (h[1], h[0]) if t % 2 == 0 else (h[0], h[1])
+        s = src[0:P] + src[1:P + 1] + src[2:P + 2]
+        dst[1:P + 1] = torch.div(s, 3, rounding_mode="trunc")
+    return torch.cat(h).int()
+
+
+def test_jacobi1d_full_size_against_torch_restatement(cuda):
+    """N = 2^28 + 2 (BASELINE configs[2]), 4 steps, full-range int32 inputs
+    (64-bit sums) and narrow inputs (32-bit sums)."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs
+
+    N, T = (1 << 28) + 2, 4
+    params = {"T": T, "N": N, "s": 16, "B": 256}
+    P = ((N - 2) // (16 * 256)) * 16 * 256
+    for lo, hi in ((-(2**31), 2**31 - 1), (-(1 << 20), 1 << 20)):
+        a = torch.randint(lo, hi, (2 * N,), dtype=torch.int32, device="cuda")
+        want = _jacobi1d_torch(a, N, T, P)
+        got = _run(programs.source("jacobi"), params, {"a": a})["a"]
+        assert torch.equal(got.reshape(-1), want)
+        del a, want, got
+        torch.cuda.empty_cache()
+
+
+def test_jacobi2d_full_size_against_torch_restatement(cuda):
+    """N = 16386 (BASELINE configs[3]), 3 steps, against a GPU restatement of
+    jacobi2d.mfk (int64 sums, truncating division)."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs
+
+    N, T = 16386, 3
+    params = {"T": T, "N": N, "s": 32, "B0": 64, "B1": 4}
+    I = ((N - 2) // 64) * 64
+    J = ((N - 2) // (32 * 4)) * 32 * 4
+    a = torch.randint(-(1 << 20), 1 << 20, (2 * N, N), dtype=torch.int32, device="cuda")
+    h = [a[:N].long(), a[N:].long()]
+    for t in range(T):
+        src, dst = (h[0], h[1]) if t % 2 == 0 else (h[1], h[0])
+        s = (src[0:I, 1:J + 1] + src[2:I + 2, 1:J + 1] + src[1:I + 1, 0:J] + src[1:I + 1, 2:J + 2] +
+             src[1:I + 1, 1:J + 1])
+        dst[1:I + 1, 1:J + 1] = torch.div(s, 5, rounding_mode="trunc")
+    want = torch.cat(h).int()
+    del h
+    got = _run(programs.source("jacobi2d"), params, {"a": a})["a"]
+    assert torch.equal(got.reshape(2 * N, N), want)
+
+
+def test_matvec_full_size_exact(cuda):
+    """N = 32768 mat-vec on small integers: the int32 result equals an exact
+    binary64 product."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs
+
+    N = 32768
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randint(-50, 50, (N, N), dtype=torch.int32, device="cuda", generator=g)
+    x = torch.randint(-50, 50, (N,), dtype=torch.int32, device="cuda", generator=g)
+    y = torch.randint(-50, 50, (N,), dtype=torch.int32, device="cuda", generator=g)
+    got = _run(programs.source("matvec"), {"N": N, "s": 1, "B": 256}, {"a": a, "x": x, "y": y})["y"]
+    want = (y.double() + a.double() @ x.double()).int()
+    assert torch.equal(got.reshape(-1), want)
