@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, binding, cases
-from .programs import FAMILIES, ProgramKind, effective_params, identify
+from .programs import FAMILIES, effective_params, identify
 
 _INT32_MIN, _INT32_MAX = -(2**31), 2**31 - 1
 
@@ -68,13 +68,11 @@ def _kind_of(value) -> str:
 
 
 def _list_dtype(data) -> str:
-    flat = data[0] if data and isinstance(data[0], list) else data
     rows = data if data and isinstance(data[0], list) else [data]
     for row in rows:
         for v in row:
             if isinstance(v, float):
                 return "f"
-    del flat
     return "i"
 
 
@@ -135,7 +133,6 @@ def _to_device_tensor(name, value, shape, np_dtype, device):
 
 
 def _from_device(t, kind: str, shape, like):
-    torch = _torch()
     if kind == "torch":
         dev = like.device if like is not None else t.device
         out = t.reshape(shape) if t.numel() == _numel(shape) else t
@@ -145,7 +142,6 @@ def _from_device(t, kind: str, shape, like):
         host = host.reshape(shape)
     if kind == "numpy":
         return host.copy()
-    del torch
     return host.tolist()
 
 
@@ -236,11 +232,7 @@ def run_program(
     else:
         applied, case_index, fallback = kind.applied, None, False
 
-    arrays = dict(arrays or {})
-    for name in arrays:
-        if name not in {a.name for a in fam.arrays}:
-            # the reference deep-copies unknown arrays through untouched
-            pass
+    arrays = dict(arrays or {})  # arrays the program does not declare come back as copies (below)
     dtypes = {_dtype_of(v) for n, v in arrays.items() if n in {a.name for a in fam.arrays}}
     if "f" in dtypes:
         if not fam.float_ok:
