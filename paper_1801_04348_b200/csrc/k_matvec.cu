@@ -121,22 +121,39 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     // lanes per row: the largest power of two <= 32 dividing the block size
     int lanes = 1;
     while (lanes < 32 && nt % (lanes * 2) == 0) lanes *= 2;
-    const int64_t blocks = ceil_div(rhi - rlo, tile);
-    if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matvec: grid too large");
     const T *a = static_cast<const T *>(p[0]);
     const T *x = static_cast<const T *>(p[1]);
     T *y = static_cast<T *>(p[2]);
     const bool vec = L.N % 4 == 0 && aligned16(a) && aligned16(x);
-    if (L.variant == PK_VARIANT_STAGED) {
-        const size_t smem = (size_t)L.N * sizeof(T);
-        const void *k = vec ? (const void *)k_matvec<T, true, true> : (const void *)k_matvec<T, true, false>;
+    const bool staged = L.variant == PK_VARIANT_STAGED;
+    const size_t smem = staged ? (size_t)L.N * sizeof(T) : 0;
+    const void *k = staged ? (vec ? (const void *)k_matvec<T, true, true> : (const void *)k_matvec<T, true, false>)
+                           : (vec ? (const void *)k_matvec<T, false, true> : (const void *)k_matvec<T, false, false>);
+    if (staged) {
         int rc = allow_smem(k, smem);
         if (rc) return rc;
-        if (vec) k_matvec<T, true, true><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
-        else k_matvec<T, true, false><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+    }
+    // Rows per block: the case's tile, or less so that every SM gets a block --
+    // the staged x (N words) allows one block per SM at N = 32768, and
+    // N / (s*B) tiles would leave SMs idle (128 of 148 at the BASELINE size).
+    int per_sm = 0, sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, smem);
+    const int64_t slots = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    const int64_t step = (int64_t)(nt / lanes) * kRows;  // rows one pass of the block's groups covers
+    int64_t rows = rhi - rlo, chunk = tile;
+    if (ceil_div(rows, chunk) < slots) chunk = ceil_div(ceil_div(rows, slots), step) * step;
+    if (chunk < 1) chunk = 1;
+    const int64_t blocks = ceil_div(rows, chunk);
+    if (blocks > 0x7fffffffLL || chunk > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matvec: grid too large");
+    const int ct = (int)chunk;
+    if (staged) {
+        if (vec) k_matvec<T, true, true><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, ct, lanes);
+        else k_matvec<T, true, false><<<(unsigned)blocks, nt, smem, st>>>(a, x, y, L.N, rlo, rhi, ct, lanes);
     } else {
-        if (vec) k_matvec<T, false, true><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
-        else k_matvec<T, false, false><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, tile, lanes);
+        if (vec) k_matvec<T, false, true><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, ct, lanes);
+        else k_matvec<T, false, false><<<(unsigned)blocks, nt, 0, st>>>(a, x, y, L.N, rlo, rhi, ct, lanes);
     }
     return after_launch("matvec");
 }
