@@ -739,6 +739,11 @@ int sweep1d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "jacobi: grid too large");
     const int vec = !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7u);
     const int mode = sweep_mode(L, flag);
+    if (L.variant == PK_VARIANT_STAGED && !(L.flags & PK_FLAG_GENERIC)) {
+        // the window staged in registers (k_jacobi_reg.cu) unless the layout is not its
+        rc = sweep1d_reg(src, dst, lo, hi, L.N, flag, mode, st);
+        if (rc != kNotTaken) return rc;
+    }
     if (L.variant == PK_VARIANT_STAGED) {
         // tiles whose whole (16-byte rounded) window lies inside the half go
         // through the TMA pipeline; the one or two edge tiles through the
@@ -801,6 +806,10 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "jacobi2d: grid too large");
     const int vec = (L.N % 2 == 0) && !((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 7u);
     const int mode = sweep_mode(L, flag);
+    if (L.variant == PK_VARIANT_STAGED && !(L.flags & PK_FLAG_GENERIC)) {
+        rc = sweep2d_reg(src, dst, lo, hi, e.J, L.N, flag, mode, st);
+        if (rc != kNotTaken) return rc;
+    }
     if (L.variant == PK_VARIANT_STAGED) {
         const size_t smem = (size_t)(TI + 2) * (size_t)(TJ + 8) * sizeof(int);
         rc = allow_smem((const void *)k_jacobi2d_staged, smem);

@@ -114,6 +114,12 @@ int jacobi1d_temporal_pass(const pk_launch_t &L, int *a, int64_t lo, int64_t hi,
                            const int *flag, int mode, cudaStream_t st);
 int jacobi2d_temporal_pass(const pk_launch_t &L, int *a, int64_t lo, int64_t hi, int64_t I, int64_t J, int64_t t0,
                            int h, const int *flag, int mode, cudaStream_t st);
+// register-window sweeps (k_jacobi_reg.cu): kNotTaken when the layout is not theirs
+constexpr int kNotTaken = -1;
+int sweep1d_reg(const int *src, int *dst, int64_t lo, int64_t hi, int64_t N, const int *flag, int mode,
+                cudaStream_t st);
+int sweep2d_reg(const int *src, int *dst, int64_t lo, int64_t hi, int64_t J, int64_t N, const int *flag, int mode,
+                cudaStream_t st);
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
 bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n);
