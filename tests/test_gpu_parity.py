@@ -251,10 +251,14 @@ def test_matmul_full_size_integer_valued_exact(cuda):
     a = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
     b = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
     c = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
-    got = _run(programs.source("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": 16}, {"a": a, "b": b, "c": c})["c"]
-    assert last_run().applied == ()
     want = c.double() + a.double() @ b.double()
-    assert torch.equal(got.reshape(n, n).double(), want)
+    # several launches: a missing proxy fence between the consumers' shared
+    # loads and the next TMA refill once corrupted one tile every few runs
+    for rep in range(4):
+        got = _run(programs.source("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": 16},
+                   {"a": a, "b": b, "c": c})["c"]
+        assert last_run().applied == ()
+        assert torch.equal(got.reshape(n, n).double(), want), rep
 
 
 def _jacobi1d_torch(a, N, T, P):
