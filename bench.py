@@ -358,6 +358,9 @@ def main() -> int:
 
     kernels = {}
     cpu = None
+    if world > 1 and not args.no_kernels:
+        del ha, hb, hc
+        kernels = bench_kernels_sharded(peaks, mv, rank, world)
     if rank == 0 and world == 1 and not args.no_kernels:
         del ha, hb, hc
         kernels = bench_kernels(peaks, mv, args.no_tune)
@@ -476,6 +479,83 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
                             "because h steps share one HBM pass; results bit-identical"}
         del bufs
         torch.cuda.empty_cache()
+    return out
+
+
+def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
+    """The bandwidth-bound BASELINE configs over all ranks (N > 1), placed by
+    the partitioner: reversal by input element, transpose / mat-vec by output
+    row (no data-path collective), the stencils by row slab with ghost zones
+    of width h refreshed every h steps by NCCL send/recv over NVLink
+    (partition.run_stencil).  GB/s of whole-job algorithmic traffic over the
+    max-over-ranks device time; the leaf parameters are each family's
+    recorded tuner pick (TUNE_GRIDS[fam][0])."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1801_04348_b200 import _lib, binding, cases, partition, programs
+
+    out = {}
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = torch.cuda.current_stream(dev)
+    for fam, (params, work, unit) in KERNEL_CONFIGS.items():
+        try:
+            kind = programs.original(fam)
+            run_params = dict(params, **TUNE_GRIDS[fam][0])
+            sel = cases.select(kind, run_params, mv)
+            shapes = programs.array_shapes(kind, run_params)
+            g = torch.Generator(device=dev)
+            g.manual_seed(0x1801)  # the same inputs on every rank
+            bufs = []
+            for arr in programs.FAMILIES[fam].arrays:
+                n = 1
+                for d in shapes[arr.name]:
+                    n *= d
+                bufs.append(torch.randint(-(1 << 20), 1 << 20, (n,), dtype=torch.int32, device=dev, generator=g))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if fam in ("jacobi", "jacobi2d"):
+                L = binding.make_launch(kind, dict(run_params, T=1), sel.applied, _lib.DTYPE_I32)
+                if _lib.jacobi_narrow(L, bufs[0].data_ptr(), st.cuda_stream):
+                    L.flags |= _lib.FLAG_NARROW
+                ex = partition.TorchExchanger()
+                plan = partition.halo_plan(fam, run_params, rank, world, width=16)
+
+                def sweep(src, dst, lo, hi, L=L):
+                    _lib.jacobi_sweep(L, src.data_ptr(), dst.data_ptr(), lo, hi, st.cuda_stream)
+
+                def run():
+                    partition.drive(partition.run_stencil(fam, run_params, bufs[0], ex, sweep, plan=plan))
+                detail = {"ghost_width": plan.width, "slab": [plan.lo, plan.hi]}
+            else:
+                lo, hi = partition.unit_range_launch(fam, run_params, rank, world)
+                L = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32, lo=lo, hi=hi)
+                ptrs = [x.data_ptr() for x in bufs]
+
+                def run(L=L, ptrs=ptrs, lo=lo, hi=hi):
+                    if hi > lo:
+                        for _ in range(5):
+                            _lib.launch(L, ptrs, st.cuda_stream)
+                detail = {"units": [lo, hi]}
+            run()  # warm-up
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record(st)
+            run()
+            e1.record(st)
+            torch.cuda.synchronize()
+            reps = 1 if fam.startswith("jacobi") else 5
+            ms = torch.tensor([e0.elapsed_time(e1) / reps], device=dev)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            ms = float(ms.item())
+            gbs = work / (ms * 1e-3) / 1e9
+            out[fam] = {"params": run_params, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
+                        "value": round(gbs, 1), "unit": unit, "n_gpus": world,
+                        "frac_of_measured_hbm_x_n": round(gbs / (peaks["hbm_gbs"] * world), 4),
+                        "placement": detail if rank == 0 else None}
+            del bufs
+            torch.cuda.empty_cache()
+        except Exception as exc:  # informative extras: never lose the headline line
+            out[fam] = {"unavailable": ("%s: %s" % (type(exc).__name__, exc))[:200]}
     return out
 
 
