@@ -552,6 +552,32 @@ def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
                         "value": round(gbs, 1), "unit": unit, "n_gpus": world,
                         "frac_of_measured_hbm_x_n": round(gbs / (peaks["hbm_gbs"] * world), 4),
                         "placement": detail if rank == 0 else None}
+            if fam in ("jacobi", "jacobi2d"):
+                # the same slabs with the halo exchange fused into the sweep: ghost units
+                # stored straight into the neighbours' buffers over NVLink (CUDA IPC), no NCCL
+                g.manual_seed(0x1801)
+                bufs[0].copy_(torch.randint(-(1 << 20), 1 << 20, bufs[0].shape, dtype=torch.int32, device=dev,
+                                            generator=g))
+                ps = partition.PeerStencil(fam, run_params, bufs[0], L)
+                ps.run(params["T"])  # warm-up
+                ps.finish()
+                ps.ctr.zero_()
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0.record(st)
+                for t in range(params["T"]):
+                    _lib.jacobi_sweep_peer(L, bufs[0].data_ptr(), t, ps.lo, ps.hi, ps.peer, st.cuda_stream)
+                e1.record(st)
+                torch.cuda.synchronize()
+                ps.close()
+                pms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+                dist.all_reduce(pms, op=dist.ReduceOp.MAX)
+                pms = float(pms.item())
+                pg = work / (pms * 1e-3) / 1e9
+                out[fam + "_peer"] = {"params": run_params, "ms": round(pms, 3), "value": round(pg, 1), "unit": unit,
+                                      "n_gpus": world, "frac_of_measured_hbm_x_n": round(pg / (peaks["hbm_gbs"] * world), 4),
+                                      "exchange": "fused into the sweep: ghost units stored into the neighbours' "
+                                                  "buffers through CUDA IPC (NVLink), device counters, no NCCL"}
             del bufs
             torch.cuda.empty_cache()
         except Exception as exc:  # informative extras: never lose the headline line

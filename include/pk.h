@@ -159,6 +159,39 @@ int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo
 int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *const *dev_ptrs, int nptrs,
                     int64_t halo, int gather);
 
+/* ---- fused halo exchange over peer memory (one process per GPU) ----------
+ * Every rank holds the whole Jacobi double buffer `a` with the program's
+ * global indexing and owns units [lo, hi) (positions / rows).  One call runs
+ * step `step` (the half parity of jacobi.mfk / jacobi2d.mfk) of the
+ * register-window sweep over [lo, hi); the blocks computing unit lo and unit
+ * hi - 1 also store those values into the left / right neighbour's buffer
+ * (the same offset through an IPC mapping: NVLink stores on an 8 x B200 box),
+ * and order themselves against the neighbours with the counters below: they
+ * wait, before loading, for the neighbour's edge blocks of step - 1, and
+ * signal after storing (system-scope fence + atomic).  Interior blocks never
+ * wait.  Counters start at 0 for step 0 (zero them, then barrier, before a
+ * run).  Replaces the NCCL ghost-zone exchange of the partitioner for the
+ * stencils (partition.PeerStencil).  Requires even N and 16-byte aligned
+ * halves for 2-D. */
+typedef struct pk_peer {
+    void *left_base, *right_base;           /* neighbours' double buffers, mapped (NULL: no neighbour) */
+    uint32_t *wait_left, *wait_right;       /* this rank's counters, bumped by the neighbours          */
+    uint32_t *signal_left, *signal_right;   /* left neighbour's wait_right / right neighbour's wait_left */
+    uint32_t *error;                        /* set to 1 when a wait gave up after ~2 s (a neighbour that
+                                               never signalled): the sweep then proceeds, results are
+                                               invalid, the caller must check it                        */
+} pk_peer_t;
+int pk_jacobi_sweep_peer(const pk_launch_t *L, void *a, int64_t step, int64_t lo, int64_t hi, const pk_peer_t *peer,
+                         void *stream);
+
+/* CUDA IPC for pk_peer_t: export a device pointer (any address inside an
+ * allocation) as a 64-byte handle plus its offset from the allocation base;
+ * open a handle exported by another process (returns base + offset); close
+ * what pk_ipc_open returned. */
+int pk_ipc_export(const void *ptr, void *handle64, int64_t *offset);
+int pk_ipc_open(const void *handle64, int64_t offset, void **ptr);
+int pk_ipc_close(void *ptr, int64_t offset);
+
 /* Value-range check for the Jacobi fast path: *narrow = 1 when every value
  * of the double buffer `a` is within the PK_FLAG_NARROW bound (a Jacobi
  * average never leaves the range of its inputs, so the bound then holds for

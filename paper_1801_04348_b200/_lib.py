@@ -55,6 +55,10 @@ EXPORTS = (
     "pk_run_host",
     "pk_launch_multi",
     "pk_jacobi_sweep",
+    "pk_jacobi_sweep_peer",
+    "pk_ipc_export",
+    "pk_ipc_open",
+    "pk_ipc_close",
     "pk_jacobi_narrow",
     "pk_footprint_words",
     "pk_launch_count",
@@ -86,6 +90,20 @@ class PkLaunch(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class PkPeer(ctypes.Structure):
+    """pk_peer_t: the neighbours of a rank for pk_jacobi_sweep_peer."""
+
+    _fields_ = [
+        ("left_base", ctypes.c_void_p),
+        ("right_base", ctypes.c_void_p),
+        ("wait_left", ctypes.c_void_p),
+        ("wait_right", ctypes.c_void_p),
+        ("signal_left", ctypes.c_void_p),
+        ("signal_right", ctypes.c_void_p),
+        ("error", ctypes.c_void_p),
+    ]
 
 
 class PkMachine(ctypes.Structure):
@@ -146,6 +164,15 @@ def load() -> ctypes.CDLL:
         lib.pk_launch_multi.restype = ctypes.c_int
         lib.pk_jacobi_sweep.argtypes = [ctypes.POINTER(PkLaunch), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
         lib.pk_jacobi_sweep.restype = ctypes.c_int
+        lib.pk_jacobi_sweep_peer.argtypes = [ctypes.POINTER(PkLaunch), vp, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.POINTER(PkPeer), vp]
+        lib.pk_jacobi_sweep_peer.restype = ctypes.c_int
+        lib.pk_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64)]
+        lib.pk_ipc_export.restype = ctypes.c_int
+        lib.pk_ipc_open.argtypes = [vp, ctypes.c_int64, ctypes.POINTER(vp)]
+        lib.pk_ipc_open.restype = ctypes.c_int
+        lib.pk_ipc_close.argtypes = [vp, ctypes.c_int64]
+        lib.pk_ipc_close.restype = ctypes.c_int
         lib.pk_jacobi_narrow.argtypes = [ctypes.POINTER(PkLaunch), vp, ctypes.POINTER(ctypes.c_int32), vp]
         lib.pk_jacobi_narrow.restype = ctypes.c_int
         lib.pk_footprint_words.argtypes = [ctypes.POINTER(PkLaunch)]
@@ -225,6 +252,32 @@ def jacobi_sweep(L: PkLaunch, src: int, dst: int, lo: int, hi: int, stream: int 
     lib = load()
     check(lib.pk_jacobi_sweep(ctypes.byref(L), ctypes.c_void_p(src), ctypes.c_void_p(dst), lo, hi,
                               ctypes.c_void_p(stream or None)))
+
+
+def jacobi_sweep_peer(L: PkLaunch, a: int, step: int, lo: int, hi: int, peer: PkPeer, stream: int = 0) -> None:
+    lib = load()
+    check(lib.pk_jacobi_sweep_peer(ctypes.byref(L), ctypes.c_void_p(a), step, lo, hi, ctypes.byref(peer),
+                                   ctypes.c_void_p(stream or None)))
+
+
+def ipc_export(ptr: int) -> tuple[bytes, int]:
+    """(64-byte handle, offset from the allocation base) of a device pointer."""
+    lib = load()
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    check(lib.pk_ipc_export(ctypes.c_void_p(ptr), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    lib = load()
+    out = ctypes.c_void_p(0)
+    check(lib.pk_ipc_open(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    check(load().pk_ipc_close(ctypes.c_void_p(ptr), offset))
 
 
 def jacobi_narrow(L: PkLaunch, a: int, stream: int = 0) -> bool:

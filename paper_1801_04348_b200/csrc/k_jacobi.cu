@@ -874,6 +874,48 @@ int sweep_jacobi2d(const pk_launch_t &L, const void *src, void *dst, int64_t lo,
     return sweep2d_impl(L, static_cast<const int *>(src), static_cast<int *>(dst), lo, hi, nullptr, st);
 }
 
+// One step t of a Jacobi program over units [lo, hi) with the neighbours'
+// ghost units written into their buffers (see PeerSweep, k_jacobi_reg.cu).
+int jacobi_sweep_peer(const pk_launch_t &L, int *a, int64_t step, int64_t lo, int64_t hi, const pk_peer_t &P,
+                      cudaStream_t st) {
+    const bool two_d = L.family == PK_FAMILY_JACOBI2D;
+    int64_t ulo = 1, uhi = 1, J = 0;
+    if (two_d) {
+        Extents2D e;
+        int rc = extents2d(L, &e);
+        if (rc) return rc;
+        uhi = e.I + 1;
+        J = e.J;
+    } else {
+        Extents1D e;
+        int rc = extents1d(L, &e);
+        if (rc) return rc;
+        uhi = e.P + 1;
+    }
+    if (lo < ulo) lo = ulo;
+    if (hi > uhi) hi = uhi;
+    const int64_t half = two_d ? L.N * L.N : L.N;
+    // 1-D: t even writes the lower half (jacobi.mfk:19-23); 2-D: t even writes the upper half
+    const bool lower_dst = two_d ? (step % 2 != 0) : (step % 2 == 0);
+    int *dst = lower_dst ? a : a + half;
+    const int *src = lower_dst ? a + half : a;
+    const int64_t off = dst - a;
+    PeerHost R;
+    R.left_dst = P.left_base ? static_cast<int *>(P.left_base) + off : nullptr;
+    R.right_dst = P.right_base ? static_cast<int *>(P.right_base) + off : nullptr;
+    R.wait_left = P.wait_left;
+    R.wait_right = P.wait_right;
+    R.sig_left = P.signal_left;
+    R.sig_right = P.signal_right;
+    R.error = P.error;
+    R.step = step;
+    if ((R.left_dst || R.right_dst) && !R.error) return fail(PK_E_PARAM, "pk_jacobi_sweep_peer: no error word");
+    if ((R.left_dst && (!R.wait_left || !R.sig_left)) || (R.right_dst && (!R.wait_right || !R.sig_right)))
+        return fail(PK_E_PARAM, "pk_jacobi_sweep_peer: a neighbour without its counters");
+    const int mode = (L.flags & PK_FLAG_NARROW) ? 1 : 0;
+    return sweep_reg_peer(two_d, src, dst, lo, hi, J, L.N, mode, R, st);
+}
+
 int jacobi_narrow(const pk_launch_t &L, const void *a, int *narrow, cudaStream_t st) {
     const bool one = L.family == PK_FAMILY_JACOBI1D;
     const int64_t n = one ? 2 * L.N : 2 * L.N * L.N;

@@ -64,6 +64,60 @@ __device__ __forceinline__ int ld1_guard(const int *a, int64_t y, int64_t n) {
 }
 __device__ __forceinline__ int q_at(const int4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
+// Fused halo exchange over peer memory (pk_jacobi_sweep_peer).  Every rank
+// holds the whole double buffer with global indexing, so the neighbours'
+// ghost point / row is written straight into their buffer (same offset,
+// through the IPC mapping: NVLink stores) by the block that computes it.
+// Ordering: a rank's edge blocks wait, before loading, until the neighbour's
+// edge blocks of the previous step have signalled (their remote stores into
+// our ghosts are done, and so are their reads of the half we are about to
+// overwrite in their buffer); after storing, they signal the neighbours with
+// a system-scope fence + atomic.  Interior blocks never wait.
+struct PeerSweep {
+    int *left_dst, *right_dst;         // neighbours' copies of this sweep's dst half (nullptr: none)
+    const unsigned *wait_left, *wait_right;  // this rank's counters
+    unsigned *sig_left, *sig_right;    // the neighbours' counters (mapped)
+    unsigned *error;                   // set when a wait gives up (a neighbour never signalled)
+    unsigned target;                   // edge blocks per step x steps already run
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// bounded spin (~2 s): a neighbour that never signals sets the error word
+// instead of hanging the device
+__device__ __forceinline__ void spin_until(const unsigned *ctr, unsigned target, unsigned *error) {
+    for (unsigned k = 0; ld_acquire_sys(ctr) < target; k++) {
+        if (k == (1u << 24)) {
+            atomicExch(error, 1u);
+            return;
+        }
+        __nanosleep(128);
+    }
+}
+
+// thread 0 waits for the neighbours this block borders, then the block proceeds
+__device__ __forceinline__ void peer_wait(const PeerSweep &P, bool left, bool right) {
+    if (threadIdx.x == 0) {
+        if (left) spin_until(P.wait_left, P.target, P.error);
+        if (right) spin_until(P.wait_right, P.target, P.error);
+    }
+    __syncthreads();
+}
+
+// after every thread of the block has stored: publish to the neighbours
+__device__ __forceinline__ void peer_signal(const PeerSweep &P, bool left, bool right) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (left) atomicAdd_system(P.sig_left, 1u);
+        if (right) atomicAdd_system(P.sig_right, 1u);
+    }
+}
+
 // ------------------------------------------------------------------ 1-D ----
 //
 // Output quads x = xa + 4q are 16-byte aligned in dst; the source quad a
@@ -74,9 +128,10 @@ __device__ __forceinline__ int q_at(const int4 &v, int i) { return i == 0 ? v.x 
 // across the warp edge themselves (an L1 hit: the neighbouring warp loads it).
 constexpr int kJ1Threads = 256, kJ1K = 2;  // K quads per thread, strided by the warp
 
-template <bool WIDE, int D, int K>
+template <bool WIDE, int D, int K, bool PEER = false>
 __device__ __forceinline__ void j1r_compute(const int4 (&own)[K], const int4 (&edge)[K], int *__restrict__ d,
-                                            int64_t xw, int64_t lo, int64_t hi, bool interior) {
+                                            int64_t xw, int64_t lo, int64_t hi, bool interior,
+                                            const PeerSweep *P = nullptr) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int j = 0; j < K; j++) {
@@ -97,6 +152,11 @@ __device__ __forceinline__ void j1r_compute(const int4 (&own)[K], const int4 (&e
         }
         const int v0 = r_avg3<WIDE>(w[0], w[1], w[2]), v1 = r_avg3<WIDE>(w[1], w[2], w[3]);
         const int v2 = r_avg3<WIDE>(w[2], w[3], w[4]), v3 = r_avg3<WIDE>(w[3], w[4], w[5]);
+        if (PEER) {  // the neighbours' ghost points: our first and last output
+            const int vv[4] = {v0, v1, v2, v3};
+            if (P->left_dst && lo >= x && lo < x + 4) P->left_dst[lo] = vv[lo - x];
+            if (P->right_dst && hi - 1 >= x && hi - 1 < x + 4) P->right_dst[hi - 1] = vv[hi - 1 - x];
+        }
         if (interior || (x >= lo && x + 4 <= hi)) {
             *reinterpret_cast<int4 *>(d + x) = make_int4(v0, v1, v2, v3);
         } else {
@@ -111,13 +171,20 @@ __device__ __forceinline__ void j1r_compute(const int4 (&own)[K], const int4 (&e
 // The loads do not depend on the sum width: they are issued first, the
 // narrow flag (a device word set by the range pre-pass) is read beside
 // them, and only the arithmetic branches on it.
-template <int D>
+template <int D, bool PEER = false>
 __global__ void __launch_bounds__(kJ1Threads) k_jacobi1d_reg(const int *__restrict__ s, int *__restrict__ d,
                                                              int64_t xa, int64_t q0, int64_t lo, int64_t hi,
-                                                             int64_t N, const int *flag, int mode) {
+                                                             int64_t N, const int *flag, int mode,
+                                                             PeerSweep P = PeerSweep{}) {
     constexpr int K = kJ1K;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t qw = q0 + ((int64_t)blockIdx.x * (kJ1Threads / 32) + warp) * 32 * K;  // warp's first quad
+    // PEER: the last block (it holds hi - 1) runs first, then block 0 (lo), so
+    // both edges are computed and signalled at the start of the sweep
+    const int64_t bx = !PEER ? (int64_t)blockIdx.x
+                             : (blockIdx.x == 0 ? (int64_t)gridDim.x - 1 : (int64_t)blockIdx.x - 1);
+    const bool pl = PEER && bx == 0 && P.left_dst, pr = PEER && bx == (int64_t)gridDim.x - 1 && P.right_dst;
+    if (PEER && (pl || pr)) peer_wait(P, pl, pr);
+    const int64_t qw = q0 + (bx * (kJ1Threads / 32) + warp) * 32 * K;  // warp's first quad
     const int64_t xw = xa + 4 * qw;
     const bool narrow = r_narrow(mode, flag);
     // warp-uniform: every load inside [0, N) and every store inside [lo, hi)
@@ -137,9 +204,10 @@ __global__ void __launch_bounds__(kJ1Threads) k_jacobi1d_reg(const int *__restri
         if (D == 0 && lane == 31) edge[j].x = interior ? __ldg(s + y + 4) : ld1_guard(s, y + 4, N);
     }
     if (narrow)
-        j1r_compute<false, D, K>(own, edge, d, xw, lo, hi, interior);
+        j1r_compute<false, D, K, PEER>(own, edge, d, xw, lo, hi, interior, &P);
     else
-        j1r_compute<true, D, K>(own, edge, d, xw, lo, hi, interior);
+        j1r_compute<true, D, K, PEER>(own, edge, d, xw, lo, hi, interior, &P);
+    if (PEER && (pl || pr)) peer_signal(P, pl, pr);
 }
 
 // ------------------------------------------------------------------ 2-D ----
@@ -162,8 +230,27 @@ struct RowQ {
 // (all but the first / last column block and the last band) run unguarded.
 // PH2: N = 2 (mod 4), loaded row u is 8-byte aligned iff u is odd.
 template <bool WIDE, bool PH2, bool EDGE>
+__device__ __forceinline__ void j2r_store(int *o, int64_t c, int64_t J, bool full, bool ph, int v0, int v1,
+                                          int v2, int v3) {
+    if (full) {
+        if (!ph) {
+            *reinterpret_cast<int4 *>(o) = make_int4(v0, v1, v2, v3);
+        } else {
+            *reinterpret_cast<int2 *>(o) = make_int2(v0, v1);
+            *reinterpret_cast<int2 *>(o + 2) = make_int2(v2, v3);
+        }
+    } else {
+        if (c >= 1 && c <= J) o[0] = v0;
+        if (c + 1 >= 1 && c + 1 <= J) o[1] = v1;
+        if (c + 2 >= 1 && c + 2 <= J) o[2] = v2;
+        if (c + 3 >= 1 && c + 3 <= J) o[3] = v3;
+    }
+}
+
+template <bool WIDE, bool PH2, bool EDGE, bool PEER = false>
 __device__ __forceinline__ void j2r_compute(const RowQ (&rows)[kJ2R + 2], int *__restrict__ d, int64_t N,
-                                            int64_t i0, int64_t c, int64_t lo, int64_t hi, int64_t J) {
+                                            int64_t i0, int64_t c, int64_t lo, int64_t hi, int64_t J,
+                                            const PeerSweep *P = nullptr) {
     const bool full = !EDGE || (c >= 1 && c + 3 <= J);
 #pragma unroll
     for (int u = 0; u < kJ2R; u++) {
@@ -175,26 +262,19 @@ __device__ __forceinline__ void j2r_compute(const RowQ (&rows)[kJ2R + 2], int *_
         const int v1 = r_avg5<WIDE>(up.q.y, dn.q.y, cur.q.x, cur.q.z, cur.q.y);
         const int v2 = r_avg5<WIDE>(up.q.z, dn.q.z, cur.q.y, cur.q.w, cur.q.z);
         const int v3 = r_avg5<WIDE>(up.q.w, dn.q.w, cur.q.z, cur.r, cur.q.w);
-        int *o = d + i * N + c;
-        if (full) {
-            if (!ph) {
-                *reinterpret_cast<int4 *>(o) = make_int4(v0, v1, v2, v3);
-            } else {
-                *reinterpret_cast<int2 *>(o) = make_int2(v0, v1);
-                *reinterpret_cast<int2 *>(o + 2) = make_int2(v2, v3);
-            }
-        } else {
-            if (c >= 1 && c <= J) o[0] = v0;
-            if (c + 1 >= 1 && c + 1 <= J) o[1] = v1;
-            if (c + 2 >= 1 && c + 2 <= J) o[2] = v2;
-            if (c + 3 >= 1 && c + 3 <= J) o[3] = v3;
+        j2r_store<WIDE, PH2, EDGE>(d + i * N + c, c, J, full, ph, v0, v1, v2, v3);
+        if (PEER) {  // the neighbours' ghost rows: our first and last output row
+            if (P->left_dst && i == lo) j2r_store<WIDE, PH2, EDGE>(P->left_dst + i * N + c, c, J, full, ph, v0, v1, v2, v3);
+            if (P->right_dst && i == hi - 1)
+                j2r_store<WIDE, PH2, EDGE>(P->right_dst + i * N + c, c, J, full, ph, v0, v1, v2, v3);
         }
     }
 }
 
-template <bool PH2, bool EDGE>
+template <bool PH2, bool EDGE, bool PEER = false>
 __device__ __forceinline__ void j2r_band(const int *__restrict__ s, int *__restrict__ d, int64_t N, int64_t i0,
-                                         int64_t c, int64_t lo, int64_t hi, int64_t J, bool narrow) {
+                                         int64_t c, int64_t lo, int64_t hi, int64_t J, bool narrow,
+                                         const PeerSweep *P = nullptr) {
     constexpr int R = kJ2R;
     const int lane = threadIdx.x & 31;
     const int nl = EDGE ? (int)min((int64_t)R + 2, hi + 1 - (i0 - 1)) : R + 2;  // rows i0-1 .. min(i0+R, hi)
@@ -250,26 +330,33 @@ __device__ __forceinline__ void j2r_band(const int *__restrict__ s, int *__restr
         }
     }
     if (narrow)
-        j2r_compute<false, PH2, EDGE>(rows, d, N, i0, c, lo, hi, J);
+        j2r_compute<false, PH2, EDGE, PEER>(rows, d, N, i0, c, lo, hi, J, P);
     else
-        j2r_compute<true, PH2, EDGE>(rows, d, N, i0, c, lo, hi, J);
+        j2r_compute<true, PH2, EDGE, PEER>(rows, d, N, i0, c, lo, hi, J, P);
 }
 
-template <bool PH2>
+template <bool PH2, bool PEER = false>
 __global__ void __launch_bounds__(kJ2Warps * 32) k_jacobi2d_reg(const int *__restrict__ s, int *__restrict__ d,
                                                                 int64_t N, int64_t rs, int64_t lo, int64_t hi,
-                                                                int64_t J, int64_t ncb, const int *flag, int mode) {
+                                                                int64_t J, int64_t ncb, const int *flag, int mode,
+                                                                PeerSweep P = PeerSweep{}) {
     const bool narrow = r_narrow(mode, flag);
-    const int64_t cb = blockIdx.x % ncb, rb = blockIdx.x / ncb;
+    const int64_t cb = blockIdx.x % ncb, rbi = blockIdx.x / ncb;
+    // PEER: the last band (it holds row hi - 1) runs first, then band 0 (row lo)
+    const int64_t nrb = gridDim.x / ncb;
+    const int64_t rb = !PEER ? rbi : (rbi == 0 ? nrb - 1 : rbi - 1);
+    const bool pl = PEER && rb == 0 && P.left_dst, pr = PEER && rb == nrb - 1 && P.right_dst;
+    if (PEER && (pl || pr)) peer_wait(P, pl, pr);
     const int64_t cblk = cb * (kJ2Warps * 128);  // first column of the block
     const int64_t c = cblk + (threadIdx.x >> 5) * 128 + 4 * (threadIdx.x & 31);
     const int64_t i0 = rs + rb * kJ2R;  // odd: loaded row u has the phase of u
     const bool interior = cblk >= 4 && cblk + kJ2Warps * 128 + 8 <= N && cblk + kJ2Warps * 128 <= J + 1 &&
                           i0 >= lo && i0 + kJ2R <= hi;
     if (interior)
-        j2r_band<PH2, false>(s, d, N, i0, c, lo, hi, J, narrow);
+        j2r_band<PH2, false, PEER>(s, d, N, i0, c, lo, hi, J, narrow, &P);
     else
-        j2r_band<PH2, true>(s, d, N, i0, c, lo, hi, J, narrow);
+        j2r_band<PH2, true, PEER>(s, d, N, i0, c, lo, hi, J, narrow, &P);
+    if (PEER && (pl || pr)) peer_signal(P, pl, pr);
 }
 
 }  // namespace
@@ -318,6 +405,57 @@ int sweep2d_reg(const int *src, int *dst, int64_t lo, int64_t hi, int64_t J, int
         k_jacobi2d_reg<false><<<(unsigned)(nrb * ncb), kJ2Warps * 32, 0, st>>>(src, dst, N, rs, lo, hi, J, ncb,
                                                                               flag, mode);
     return after_launch("jacobi2d_reg");
+}
+
+// Fused sweep + halo exchange: the register-window sweep with the edge
+// blocks storing into the neighbours' buffers and ordering against them.
+// R: remote dst halves already offset; counters; steps run so far.
+int sweep_reg_peer(bool two_d, const int *src, int *dst, int64_t lo, int64_t hi, int64_t J, int64_t N, int mode,
+                   const PeerHost &R, cudaStream_t st) {
+    if (hi <= lo) return PK_OK;
+    PeerSweep P;
+    P.left_dst = R.left_dst;
+    P.right_dst = R.right_dst;
+    P.wait_left = R.wait_left;
+    P.wait_right = R.wait_right;
+    P.sig_left = R.sig_left;
+    P.sig_right = R.sig_right;
+    P.error = R.error;
+    if (!two_d) {
+        if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3u) != 0)
+            return fail(PK_E_UNSUPPORTED, "jacobi peer sweep: halves not 4-byte aligned");
+        const int so = (int)((reinterpret_cast<uintptr_t>(src) >> 2) & 3);
+        const int dof = (int)((reinterpret_cast<uintptr_t>(dst) >> 2) & 3);
+        const int64_t xa = (4 - dof) & 3;
+        const int D = (dof - so) & 3;
+        const int64_t q0 = (lo - xa) >= 0 ? (lo - xa) / 4 : -((xa - lo + 3) / 4);
+        const int64_t q1 = (hi - 1 - xa) >= 0 ? (hi - 1 - xa) / 4 : -1;
+        const int64_t blocks = ceil_div(q1 - q0 + 1, (int64_t)kJ1Threads * kJ1K);
+        if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "jacobi: grid too large");
+        P.target = (unsigned)(1 * R.step);  // one edge block per side and step
+        switch (D) {
+        case 0: k_jacobi1d_reg<0, true><<<(unsigned)blocks, kJ1Threads, 0, st>>>(src, dst, xa, q0, lo, hi, N, nullptr, mode, P); break;
+        case 1: k_jacobi1d_reg<1, true><<<(unsigned)blocks, kJ1Threads, 0, st>>>(src, dst, xa, q0, lo, hi, N, nullptr, mode, P); break;
+        case 2: k_jacobi1d_reg<2, true><<<(unsigned)blocks, kJ1Threads, 0, st>>>(src, dst, xa, q0, lo, hi, N, nullptr, mode, P); break;
+        default: k_jacobi1d_reg<3, true><<<(unsigned)blocks, kJ1Threads, 0, st>>>(src, dst, xa, q0, lo, hi, N, nullptr, mode, P); break;
+        }
+        return after_launch("jacobi1d_reg_peer");
+    }
+    if ((N & 1) || !aligned16(src) || !aligned16(dst))
+        return fail(PK_E_UNSUPPORTED, "jacobi2d peer sweep: needs even N and 16-byte aligned halves");
+    if (J <= 0) return PK_OK;
+    const int64_t rs = (lo & 1) ? lo : lo - 1;
+    const int64_t nrb = ceil_div(hi - rs, kJ2R);
+    const int64_t ncb = ceil_div((J + 1 + 3) / 4, 32 * kJ2Warps);
+    if (nrb * ncb > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "jacobi2d: grid too large");
+    P.target = (unsigned)(ncb * R.step);  // one band of ncb edge blocks per side and step
+    if ((N & 3) == 2)
+        k_jacobi2d_reg<true, true><<<(unsigned)(nrb * ncb), kJ2Warps * 32, 0, st>>>(src, dst, N, rs, lo, hi, J, ncb,
+                                                                                   nullptr, mode, P);
+    else
+        k_jacobi2d_reg<false, true><<<(unsigned)(nrb * ncb), kJ2Warps * 32, 0, st>>>(src, dst, N, rs, lo, hi, J, ncb,
+                                                                                    nullptr, mode, P);
+    return after_launch("jacobi2d_reg_peer");
 }
 
 }  // namespace pk

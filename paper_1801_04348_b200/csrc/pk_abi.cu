@@ -166,7 +166,7 @@ using namespace pk;
 
 extern "C" {
 
-int pk_version(void) { return (1 << 16) | 0; }
+int pk_version(void) { return (1 << 16) | 1; }  // 1.1: pk_jacobi_sweep_peer, pk_ipc_*
 
 const char *pk_last_error(void) { return t_err; }
 
@@ -221,6 +221,64 @@ int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo
     if (L->family == PK_FAMILY_JACOBI1D) return sweep_jacobi1d(*L, src, dst, lo, hi, st);
     if (L->family == PK_FAMILY_JACOBI2D) return sweep_jacobi2d(*L, src, dst, lo, hi, st);
     return fail(PK_E_PARAM, "pk_jacobi_sweep: family %d is not a Jacobi stencil", L->family);
+}
+
+int pk_jacobi_sweep_peer(const pk_launch_t *L, void *a, int64_t step, int64_t lo, int64_t hi, const pk_peer_t *peer,
+                         void *stream) {
+    if (!L || !a || !peer) return fail(PK_E_PARAM, "null argument");
+    if (L->family != PK_FAMILY_JACOBI1D && L->family != PK_FAMILY_JACOBI2D)
+        return fail(PK_E_PARAM, "pk_jacobi_sweep_peer: family %d is not a Jacobi stencil", L->family);
+    if (L->dtype != PK_DTYPE_I32) return fail(PK_E_UNSUPPORTED, "pk_jacobi_sweep_peer: int32 only");
+    if (step < 0 || step >= ((int64_t)1 << 31)) return fail(PK_E_PARAM, "pk_jacobi_sweep_peer: step out of range");
+    return jacobi_sweep_peer(*L, static_cast<int *>(a), step, lo, hi, *peer, static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+typedef int (*AddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
+}
+
+int pk_ipc_export(const void *ptr, void *handle64, int64_t *offset) {
+    if (!ptr || !handle64 || !offset) return fail(PK_E_PARAM, "null argument");
+    // the allocation base (cudaIpcGetMemHandle takes a base pointer; torch's
+    // caching allocator hands out addresses inside larger blocks)
+    static const AddressRangeFn range = []() -> AddressRangeFn {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<AddressRangeFn>(p);
+        return nullptr;
+    }();
+    if (!range) return fail(PK_E_CUDA, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)reinterpret_cast<uintptr_t>(ptr)) != 0)
+        return fail(PK_E_PARAM, "pk_ipc_export: not a device allocation");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - base);
+    return PK_OK;
+}
+
+int pk_ipc_open(const void *handle64, int64_t offset, void **ptr) {
+    if (!handle64 || !ptr || offset < 0) return fail(PK_E_PARAM, "bad argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    *ptr = static_cast<char *>(base) + offset;
+    return PK_OK;
+}
+
+int pk_ipc_close(void *ptr, int64_t offset) {
+    if (!ptr || offset < 0) return fail(PK_E_PARAM, "bad argument");
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<char *>(ptr) - offset);
+    if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return PK_OK;
 }
 
 int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void *stream) {

@@ -120,6 +120,18 @@ int sweep1d_reg(const int *src, int *dst, int64_t lo, int64_t hi, int64_t N, con
                 cudaStream_t st);
 int sweep2d_reg(const int *src, int *dst, int64_t lo, int64_t hi, int64_t J, int64_t N, const int *flag, int mode,
                 cudaStream_t st);
+// fused sweep + halo exchange over peer memory (k_jacobi_reg.cu)
+struct PeerHost {
+    int *left_dst, *right_dst;               // neighbours' dst halves, mapped (nullptr: none)
+    const unsigned *wait_left, *wait_right;  // this rank's counters
+    unsigned *sig_left, *sig_right;          // neighbours' counters, mapped
+    unsigned *error;                         // set by a wait that gave up
+    int64_t step;                            // steps run since the counters were zeroed
+};
+int sweep_reg_peer(bool two_d, const int *src, int *dst, int64_t lo, int64_t hi, int64_t J, int64_t N, int mode,
+                   const PeerHost &R, cudaStream_t st);
+int jacobi_sweep_peer(const pk_launch_t &L, int *a, int64_t step, int64_t lo, int64_t hi, const pk_peer_t &P,
+                      cudaStream_t st);
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
 bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n);

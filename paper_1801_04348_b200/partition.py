@@ -233,6 +233,81 @@ def drive_local(gens):
         alive = nxt
 
 
+class PeerStencil:
+    """T steps of a Jacobi program with the halo exchange fused into the sweep
+    (pk_jacobi_sweep_peer): one process per GPU, every rank holding the whole
+    double buffer ``a`` (global indexing) and owning ``split(...)``'s units.
+    The blocks that compute a rank's first / last unit also store it into the
+    neighbour's buffer through a CUDA IPC mapping (NVLink peer stores between
+    B200s) and order themselves against the neighbour with counters in device
+    memory -- no NCCL call, no separate exchange step, ghost width 1.
+
+    ``group``: any torch.distributed group (gloo or NCCL) used once to trade
+    IPC handles; ``launch``: the pk_launch_t of the selected leaf.
+    """
+
+    def __init__(self, family: str, P: dict, a, launch, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if family not in ("jacobi", "jacobi2d"):
+            raise ValueError("PeerStencil: %s is not a Jacobi stencil" % family)
+        self._lib, self._torch, self._dist = _lib, torch, dist
+        self.family, self.P, self.a, self.L, self.group = family, P, a, launch, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.lo, self.hi = split(family, P, self.rank, self.world)
+        # [from_left, from_right, error] in this rank's memory
+        self.ctr = torch.zeros(3, dtype=torch.int32, device=a.device)
+        mine = (_lib.ipc_export(a.data_ptr()), _lib.ipc_export(self.ctr.data_ptr()))
+        every = [None] * self.world
+        dist.all_gather_object(every, mine, group=group)
+        self._opened = []
+        peer = _lib.PkPeer()
+        base = self.ctr.data_ptr()
+        peer.wait_left, peer.wait_right, peer.error = base, base + 4, base + 8
+        if self.rank > 0:
+            (ha, oa), (hc, oc) = every[self.rank - 1]
+            peer.left_base = self._open(ha, oa)
+            peer.signal_left = self._open(hc, oc) + 4  # the left neighbour's from_right
+        if self.rank < self.world - 1:
+            (ha, oa), (hc, oc) = every[self.rank + 1]
+            peer.right_base = self._open(ha, oa)
+            peer.signal_right = self._open(hc, oc)  # the right neighbour's from_left
+        self.peer = peer
+
+    def _open(self, handle: bytes, offset: int) -> int:
+        ptr = self._lib.ipc_open(handle, offset)
+        self._opened.append((ptr, offset))
+        return ptr
+
+    def run(self, T: int, stream=None) -> None:
+        """Steps 0..T-1 (counters zeroed and every rank synchronised first)."""
+        torch, dist = self._torch, self._dist
+        self.ctr.zero_()
+        torch.cuda.synchronize(self.a.device)
+        dist.barrier(group=self.group)
+        st = stream if stream is not None else torch.cuda.current_stream(self.a.device).cuda_stream
+        for t in range(T):
+            self._lib.jacobi_sweep_peer(self.L, self.a.data_ptr(), t, self.lo, self.hi, self.peer, st)
+
+    def finish(self) -> None:
+        """Wait for every rank (neighbours may still be storing into our buffer)
+        and raise if a wait gave up."""
+        torch, dist = self._torch, self._dist
+        torch.cuda.synchronize(self.a.device)
+        dist.barrier(group=self.group)
+        if int(self.ctr[2].item()) != 0:
+            raise RuntimeError("PeerStencil: a neighbour never signalled (wait timed out)")
+
+    def close(self) -> None:
+        self.finish()
+        for ptr, off in self._opened:
+            self._lib.ipc_close(ptr, off)
+        self._opened = []
+
+
 # ------------------------------------------------------- row-sharded runs --
 
 # operands every rank needs whole (SURVEY 8(e): matmul's b, mat-vec's x, the
@@ -356,5 +431,5 @@ def unit_range_launch(family: str, P: dict, rank: int, world: int) -> tuple[int,
 __all__ = [
     "units", "split", "halo_plan", "run_stencil", "drive", "drive_local", "TorchExchanger",
     "LocalExchanger", "Exchanger", "unit_range_launch", "ROW_FAMILIES", "programs",
-    "REPLICATED", "share_range", "run_rows", "pk_launcher", "SHARDED_FAMILIES",
+    "REPLICATED", "share_range", "run_rows", "pk_launcher", "SHARDED_FAMILIES", "PeerStencil",
 ]

@@ -78,3 +78,19 @@ def test_temporal_jacobi2d_wide_values(cuda, oracle_mod):
     want = oracle_mod.run("jacobi2d", params, {"a": a})["a"]
     got = run_program(programs.source("jacobi2d"), params, {"a": a}, temporal=5)["a"]
     assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+
+
+def test_temporal_jacobi1d_full_size_matches_per_step(cuda):
+    """N = 2^28 + 2 (BASELINE configs[2]): the register-resident h = 15 passes
+    and the per-step sweeps leave identical double buffers (T = 37: two
+    15-step passes, a 5-step pass and the closing sweep)."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs, run_program
+
+    N = (1 << 28) + 2
+    params = {"T": 37, "N": N, "s": 16, "B": 256}
+    g = torch.Generator(device="cuda").manual_seed(99)
+    a = torch.randint(-(1 << 20), 1 << 20, (2 * N,), dtype=torch.int32, device="cuda", generator=g)
+    want = run_program(programs.source("jacobi"), params, {"a": a})["a"]
+    got = run_program(programs.source("jacobi"), params, {"a": a}, temporal=15)["a"]
+    assert torch.equal(got, want)
