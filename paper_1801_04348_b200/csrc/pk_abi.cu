@@ -1,6 +1,7 @@
 // pk_abi.cu -- the C ABI of libpk (include/pk.h): device-property lookup,
 // validation, dispatch to the family launchers, and the host-buffer path.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -311,7 +312,7 @@ bool chunkable(const pk_launch_t &L) {
 constexpr int kSlices = 4;  // reduction slices of matmul's first row chunk
 
 struct HostRun {
-    cudaStream_t h2d = nullptr, d2h = nullptr, cs[2] = {nullptr, nullptr};
+    cudaStream_t h2d = nullptr, d2h = nullptr, cs[kMaxChunks] = {};
     cudaEvent_t ev[2 * kMaxChunks + kSlices] = {};
     void *dev[3] = {nullptr, nullptr, nullptr};
 };
@@ -351,12 +352,18 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
 
     HostRun R;
     rc = PK_OK;
+    const bool trace = getenv("PK_RUN_HOST_TRACE") != nullptr;
     e = cudaStreamCreateWithFlags(&R.h2d, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.d2h, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[0], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&R.cs[1], cudaStreamNonBlocking);
+    for (int k = 0; k < nchunks && k < kMaxChunks && e == cudaSuccess; k++)
+        e = cudaStreamCreateWithFlags(&R.cs[k], cudaStreamNonBlocking);
     for (int k = 0; k < 2 * nchunks + kSlices && e == cudaSuccess; k++)
-        e = cudaEventCreateWithFlags(&R.ev[k], cudaEventDisableTiming);
+        e = cudaEventCreateWithFlags(&R.ev[k], trace ? cudaEventDefault : cudaEventDisableTiming);
+    cudaEvent_t t0ev = nullptr;
+    if (trace && e == cudaSuccess) {  // PK_RUN_HOST_TRACE=1: print each event's time (development aid)
+        cudaEventCreate(&t0ev);
+        cudaEventRecord(t0ev, R.h2d);
+    }
     if (e != cudaSuccess) rc = fail(PK_E_CUDA, "stream/event setup: %s", cudaGetErrorString(e));
 
     auto chunk = [&](int k) {
@@ -386,9 +393,11 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     if (rc == PK_OK && nchunks > 1 && L->family == PK_FAMILY_MATMUL && L->B0 > 0) {
         Kred = (N / L->B0) * L->B0;
         slice = Kred / kSlices / 128 * 128;
-        if (slice <= 0 || !matmul_kslice_ok(chunk(0), slice) ||
-            !matmul_kslice_ok(chunk(0), Kred - (kSlices - 1) * slice))
-            slice = 0;
+        // every chunk that runs slice by slice must take the sliced leaf
+        for (int r = 0; r < nchunks && r < kSlices - 1 && slice > 0; r++)
+            if (!matmul_kslice_ok(chunk(r), slice) || !matmul_kslice_ok(chunk(r), Kred - (kSlices - 1) * slice))
+                slice = 0;
+        if (slice < 0) slice = 0;
     }
     auto up_range = [&](int i, int64_t off, int64_t cnt) -> int {
         char *d = static_cast<char *>(R.dev[i]) + off * 4;
@@ -415,9 +424,63 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
                                         cudaMemcpyDeviceToHost, R.d2h);
         return x == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(x));
     };
-    for (int i = 0; i < spec.count && rc == PK_OK; i++)
-        if (whole[i] && !(slice && i == 1)) rc = up(nchunks == 1 ? *L : chunk(0), i);
-    for (int k = 0; k < nchunks && rc == PK_OK; k++) {
+    if (slice && rc == PK_OK) {
+        // Matmul: uploads interleaved so the kernels start after 2 x 64 MB and
+        // never idle while PCIe is the bottleneck.  h2d order: b_0, ac_0, b_1,
+        // ac_1, ..., b_{S-1}, ac_{S-1}, ac_S, ... (b_j: rows of b for reduction
+        // slice j; ac_r: row chunk r of a and c).  Block (r, j) runs on chunk
+        // r's own stream (slices of a chunk stay in k order: c is the fp32
+        // accumulator between them, so the bits equal one launch) as soon as
+        // b_j and ac_r are both up; chunks whose upload follows every b slice
+        // run as one full-reduction launch.  Chunk r's rows of c come down on
+        // the d2h stream after its last block.
+        auto slice_end = [&](int j) { return j + 1 < kSlices ? (int64_t)(j + 1) * slice : Kred; };
+        auto launch_block = [&](int r, int j) -> int {
+            return launch_matmul_kslice(chunk(r), R.dev, (int64_t)j * slice, slice_end(j), R.cs[r]);
+        };
+        auto finish_chunk = [&](int r) -> int {
+            cudaEventRecord(R.ev[kSlices + nchunks + r], R.cs[r]);
+            cudaStreamWaitEvent(R.d2h, R.ev[kSlices + nchunks + r], 0);
+            return down(chunk(r), 2);
+        };
+        // the transfer list: (b_j, ac_j) pairs, then the remaining chunks
+        int order[kSlices + kMaxChunks][2], nt = 0;  // {0: b_j | 1: ac_r, index}
+        for (int j = 0; j < kSlices; j++) {
+            order[nt][0] = 0, order[nt][1] = j, nt++;
+            if (j < nchunks) order[nt][0] = 1, order[nt][1] = j, nt++;
+        }
+        for (int r = kSlices; r < nchunks; r++) order[nt][0] = 1, order[nt][1] = r, nt++;
+        for (int t = 0; t < nt && rc == PK_OK; t++) {
+            if (order[t][0] == 0) {
+                const int j = order[t][1];
+                const int64_t r1 = j + 1 < kSlices ? (int64_t)(j + 1) * slice : N;  // b's rows of slice j
+                rc = up_range(1, (int64_t)j * slice * N, (r1 - (int64_t)j * slice) * N);
+                cudaEventRecord(R.ev[t], R.h2d);
+                const int up_chunks = j < nchunks ? j : nchunks;  // ac_q precedes b_j for q < j
+                for (int q = 0; q < up_chunks && rc == PK_OK; q++) {
+                    cudaStreamWaitEvent(R.cs[q], R.ev[t], 0);
+                    rc = launch_block(q, j);
+                    if (rc == PK_OK && j == kSlices - 1) rc = finish_chunk(q);
+                }
+            } else {
+                const int r = order[t][1];
+                const pk_launch_t C = chunk(r);
+                rc = up(C, 0);
+                if (rc == PK_OK) rc = up(C, 2);
+                cudaEventRecord(R.ev[t], R.h2d);
+                cudaStreamWaitEvent(R.cs[r], R.ev[t], 0);
+                if (r >= kSlices - 1) {  // every slice of b is up: one launch
+                    if (rc == PK_OK) rc = dispatch(C, R.dev, R.cs[r]);
+                    if (rc == PK_OK) rc = finish_chunk(r);
+                } else {
+                    for (int q = 0; q <= r && rc == PK_OK; q++) rc = launch_block(r, q);
+                }
+            }
+        }
+    }
+    for (int i = 0; i < spec.count && rc == PK_OK && !slice; i++)
+        if (whole[i]) rc = up(nchunks == 1 ? *L : chunk(0), i);
+    for (int k = 0; k < nchunks && rc == PK_OK && !slice; k++) {
         const pk_launch_t C = chunk(k);
         for (int i = 0; i < spec.count && rc == PK_OK; i++)
             if (!whole[i]) rc = up(C, i);
@@ -425,19 +488,7 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         cudaEventRecord(R.ev[2 * k], R.h2d);
         cudaStream_t cs = R.cs[k & 1];
         cudaStreamWaitEvent(cs, R.ev[2 * k], 0);
-        if (k == 0 && slice) {
-            for (int j = 0; j < kSlices && rc == PK_OK; j++) {  // b's rows (k) slice by slice
-                const int64_t r0 = j * slice, r1 = j + 1 < kSlices ? (j + 1) * slice : N;
-                rc = up_range(1, r0 * N, (r1 - r0) * N);
-                cudaEventRecord(R.ev[2 * nchunks + j], R.h2d);
-            }
-            for (int j = 0; j < kSlices && rc == PK_OK; j++) {
-                cudaStreamWaitEvent(cs, R.ev[2 * nchunks + j], 0);
-                rc = launch_matmul_kslice(C, R.dev, j * slice, j + 1 < kSlices ? (j + 1) * slice : Kred, cs);
-            }
-        } else {
-            rc = dispatch(C, R.dev, cs);
-        }
+        rc = dispatch(C, R.dev, cs);
         if (rc) break;
         cudaEventRecord(R.ev[2 * k + 1], cs);
         cudaStreamWaitEvent(R.d2h, R.ev[2 * k + 1], 0);
@@ -449,18 +500,33 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     for (int i = 0; i < spec.count && rc == PK_OK; i++)
         if (whole[i] && nchunks > 1) rc = down(*L, i);
     cudaError_t se = cudaSuccess;
-    for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h}) {
+    for (cudaStream_t s : R.cs) {
+        if (!s) continue;
+        cudaError_t x = cudaStreamSynchronize(s);
+        if (se == cudaSuccess) se = x;
+    }
+    for (cudaStream_t s : {R.h2d, R.d2h}) {
         if (!s) continue;
         cudaError_t x = cudaStreamSynchronize(s);
         if (se == cudaSuccess) se = x;
     }
     if (se != cudaSuccess && rc == PK_OK) rc = fail(PK_E_CUDA, "kernel execution: %s", cudaGetErrorString(se));
+    if (t0ev) {
+        for (int k = 0; k < 2 * kMaxChunks + kSlices; k++) {
+            float ms = -1.f;
+            if (R.ev[k] && cudaEventElapsedTime(&ms, t0ev, R.ev[k]) == cudaSuccess)
+                fprintf(stderr, "pk_run_host trace: event %2d at %8.3f ms\n", k, ms);
+        }
+        cudaEventDestroy(t0ev);
+    }
     for (int i = 0; i < spec.count; i++)
         if (R.dev[i]) cudaFreeAsync(R.dev[i], R.d2h);
     if (R.d2h) cudaStreamSynchronize(R.d2h);
     for (cudaEvent_t ev : R.ev)
         if (ev) cudaEventDestroy(ev);
-    for (cudaStream_t s : {R.h2d, R.cs[0], R.cs[1], R.d2h})
+    for (cudaStream_t s : R.cs)
+        if (s) cudaStreamDestroy(s);
+    for (cudaStream_t s : {R.h2d, R.d2h})
         if (s) cudaStreamDestroy(s);
     return rc;
 }

@@ -135,6 +135,9 @@ def test_run_host_shares_reassemble_oracle(cuda, oracle_mod, family, params):
 @pytest.mark.parametrize("family,params,share", [
     ("matmul", {"n": 4096, "B0": 128, "ub1": 8, "s": 16}, None),
     ("matmul", {"n": 4096, "B0": 128, "ub1": 8, "s": 16}, (1000, 3001)),
+    ("matmul", {"n": 8192, "B0": 128, "ub1": 8, "s": 16}, None),   # 8 chunks x 4 reduction slices
+    ("matmul", {"n": 2048, "B0": 128, "ub1": 8, "s": 16}, None),   # fewer chunks than slices
+    ("matmul", {"n": 8192, "B0": 128, "ub1": 8, "s": 16}, (256, 5888)),
     ("reverse", {"N": 1 << 25, "s": 16, "B": 256}, None),
     ("reverse", {"N": 1 << 25, "s": 16, "B": 256}, (12345, 30000000)),
     ("matvec", {"N": 8192, "s": 1, "B": 256}, None),
