@@ -205,6 +205,195 @@ __global__ void __launch_bounds__(kT2Threads) k_jacobi2d_temporal(const int *__r
         t2_run<true>(src, dst, half0, half1, G, t0, ntiles, sh, sh + bw);
 }
 
+// ---------------------------------------------------------------------------
+// Register wavefront (the default; the shared-memory pass above remains for
+// odd N, misaligned halves and PK_FLAG_GENERIC).  A warp owns a 128-column
+// window (a column quad per lane) and walks down a band of kWfR output rows
+// plus h halo rows above and below, one input row at a time.  Level k of the
+// pipeline holds the last two rows it produced (A_k, B_k: 2h int4 registers
+// per thread); each new level-k row n completes level k+1's row above it,
+// avg5(A_k, B_k, n, left / right of B_k by shuffle), so one input row
+// advances every level by one row and leaves level h (the pass's last step)
+// h rows behind.  No shared memory, no barriers; every step of every point
+// costs two shuffles per quad, two IADD3s and the /5.  Columns within H4
+// (h rounded up to 4) of the window edges go stale and are not stored:
+// windows overlap by 2 x H4 columns.  Rows of an N = 2 (mod 4) matrix
+// alternate 16- / 8-byte alignment; an 8-byte row is loaded as the aligned
+// quad c+2..c+5 and shifted by a shuffle (lane 0 loads its own c-2..c+1).
+// Points the program never writes (row 0, rows > I, column 0, columns > J)
+// take half d(t)'s value at each level, on warps whose window reaches them.
+constexpr int kWfR = 128;    // output rows per band
+#ifndef PK_WF_MINB
+#define PK_WF_MINB 1
+#endif
+constexpr int kWfWarps = 4;  // warps per block
+
+__device__ __forceinline__ int4 ldg4(const int *p) { return __ldg(reinterpret_cast<const int4 *>(p)); }
+
+__device__ __forceinline__ int4 ldg4_guard(const int *row, int64_t c, int64_t N) {
+    if (c >= 0 && c + 3 < N) return ldg4(row + c);
+    int v[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) v[e] = (c + e >= 0 && c + e < N) ? __ldg(row + c + e) : 0;
+    return make_int4(v[0], v[1], v[2], v[3]);
+}
+
+// input row r: the aligned quad (and lane 0's extra quad on an 8-byte row)
+template <bool PH, bool EDGE>
+__device__ __forceinline__ void wf_load(const int *src, int64_t N, int64_t r, int64_t c, int lane, int4 &raw,
+                                        int4 &ext) {
+    if (EDGE && (r < 0 || r >= N)) {
+        raw = ext = make_int4(0, 0, 0, 0);
+        return;
+    }
+    const int *row = src + r * N;
+    if (!EDGE) {
+        raw = ldg4(row + c + (PH ? 2 : 0));
+        if (PH && lane == 0) ext = ldg4(row + c - 2);
+    } else {
+        raw = ldg4_guard(row, c + (PH ? 2 : 0), N);
+        if (PH && lane == 0) ext = ldg4_guard(row, c - 2, N);
+    }
+}
+
+// the row's quad at columns c .. c+3
+template <bool PH>
+__device__ __forceinline__ int4 wf_align(const int4 &raw, const int4 &ext, int lane) {
+    if (!PH) return raw;
+    int pz = __shfl_up_sync(0xffffffffu, raw.z, 1), pw = __shfl_up_sync(0xffffffffu, raw.w, 1);
+    if (lane == 0) {
+        pz = ext.z;
+        pw = ext.w;
+    }
+    return make_int4(pz, pw, raw.x, raw.y);
+}
+
+struct WfGeom {
+    const int *src, *half0, *half1;
+    int *dst;
+    int64_t N, I, J, lo, hi, t0;
+    int64_t rs;       // first band's first output row (odd)
+    int64_t nbands, nwin;
+    int TJ;           // output columns per window
+};
+
+// One input row n (row r) through the h levels; level h's row r - h is stored.
+// (Measured alternatives, h = 7, 16386^2: shuffling a row's neighbours when
+// it is produced instead of when it is the centre -- 10.6 ms; one row per
+// iteration with two in flight -- 14.8 ms; this pair-unrolled form -- 9.3 ms.)
+template <int H, bool WIDE, bool EDGE, bool PH2>
+__device__ __forceinline__ void wf_row(int4 (&A)[H], int4 (&B)[H], int4 n, int64_t r, int64_t c, int lane,
+                                       int64_t slo, int64_t shi, const WfGeom &G) {
+#pragma unroll
+    for (int k = 0; k < H; k++) {
+        // level k: A = row r-k-2, B = row r-k-1, n = row r-k -> level k+1, row i = r-k-1
+        const int l = __shfl_up_sync(0xffffffffu, B[k].w, 1), rr = __shfl_down_sync(0xffffffffu, B[k].x, 1);
+        int4 o = make_int4(avg5<WIDE>(A[k].x, n.x, l, B[k].y, B[k].x), avg5<WIDE>(A[k].y, n.y, B[k].x, B[k].z, B[k].y),
+                           avg5<WIDE>(A[k].z, n.z, B[k].y, B[k].w, B[k].z), avg5<WIDE>(A[k].w, n.w, B[k].z, rr, B[k].w));
+        if (EDGE) {
+            const int64_t i = r - k - 1;
+            if (i < 1 || i > G.I || c < 1 || c + 3 > G.J) {  // points the program never writes: d(t)'s value
+                const int *fh = ((G.t0 + k) % 2 == 0) ? G.half1 : G.half0;  // t even writes a[N+i][j]
+                const bool row_fixed = i < 1 || i > G.I;
+                auto fix = [&](int v, int64_t j) {
+                    if (!row_fixed && j >= 1 && j <= G.J) return v;
+                    return (i >= 0 && i < G.N && j >= 0 && j < G.N) ? fh[i * G.N + j] : 0;
+                };
+                o = make_int4(fix(o.x, c), fix(o.y, c + 1), fix(o.z, c + 2), fix(o.w, c + 3));
+            }
+        }
+        A[k] = B[k];
+        B[k] = n;
+        n = o;
+    }
+    constexpr int H4 = (H + 3) & ~3;
+    const int64_t i = r - H;
+    if (i >= slo && i < shi && lane >= H4 / 4 && lane < 32 - H4 / 4) {
+        int *o = G.dst + i * G.N + c;
+        const bool ph = PH2 && (i & 1);
+        if (!EDGE || (c >= 1 && c + 3 <= G.J)) {
+            if (!ph) {
+                *reinterpret_cast<int4 *>(o) = n;
+            } else {
+                *reinterpret_cast<int2 *>(o) = make_int2(n.x, n.y);
+                *reinterpret_cast<int2 *>(o + 2) = make_int2(n.z, n.w);
+            }
+        } else {
+            if (c >= 1 && c <= G.J) o[0] = n.x;
+            if (c + 1 >= 1 && c + 1 <= G.J) o[1] = n.y;
+            if (c + 2 >= 1 && c + 2 <= G.J) o[2] = n.z;
+            if (c + 3 >= 1 && c + 3 <= G.J) o[3] = n.w;
+        }
+    }
+}
+
+template <int H, bool WIDE, bool EDGE, bool PH2>
+__device__ __forceinline__ void wf_warp(const WfGeom &G, int64_t r0, int64_t wc0) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = wc0 + 4 * lane;
+    const int64_t slo = max(max(r0, G.lo), (int64_t)1), shi = min(min(r0 + kWfR, G.hi), G.I + 1);
+    int4 A[H], B[H];
+#pragma unroll
+    for (int k = 0; k < H; k++) A[k] = B[k] = make_int4(0, 0, 0, 0);
+    // input rows r0 - H (even) .. r0 + kWfR - 1 + H (odd), in pairs: even rows at phase 0, odd at PH2
+    const int64_t rfirst = r0 - H, rlast = r0 + kWfR - 1 + H;
+    int4 rawE, extE = make_int4(0, 0, 0, 0), rawO, extO = make_int4(0, 0, 0, 0);
+    wf_load<false, EDGE>(G.src, G.N, rfirst, c, lane, rawE, extE);
+    wf_load<PH2, EDGE>(G.src, G.N, rfirst + 1, c, lane, rawO, extO);
+    for (int64_t r = rfirst; r <= rlast; r += 2) {
+        const int4 cE = rawE, cO = rawO, xO = extO;
+        if (r + 2 <= rlast) {  // the next pair in flight while this one runs through the levels
+            wf_load<false, EDGE>(G.src, G.N, r + 2, c, lane, rawE, extE);
+            wf_load<PH2, EDGE>(G.src, G.N, r + 3, c, lane, rawO, extO);
+        }
+        wf_row<H, WIDE, EDGE, PH2>(A, B, cE, r, c, lane, slo, shi, G);
+        wf_row<H, WIDE, EDGE, PH2>(A, B, wf_align<PH2>(cO, xO, lane), r + 1, c, lane, slo, shi, G);
+    }
+}
+
+// One kernel per sum width: registers are allocated for the widest path a
+// kernel contains, and the 64-bit one would cost the narrow one occupancy.
+// Under a device flag (mode 2) both are launched and the one that does not
+// match returns at once.
+template <int H, bool WIDE, bool PH2>
+__global__ void __launch_bounds__(kWfWarps * 32, PK_WF_MINB) k_jacobi2d_wavefront(WfGeom G, const int *flag, int mode) {
+    const int64_t w = (int64_t)blockIdx.x * kWfWarps + (threadIdx.x >> 5);
+    if (w >= G.nbands * G.nwin) return;  // warp-uniform
+    if (mode == 2) {
+        int v;
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((v != 0) == WIDE) return;
+    }
+    // windows of a band side by side (consecutive warps share rows in L2)
+    const int64_t band = w / G.nwin, win = w - band * G.nwin;
+    constexpr int H4 = (H + 3) & ~3;
+    const int64_t r0 = G.rs + band * kWfR, wc0 = win * G.TJ - H4;
+    // edge: some row of the cone outside 1..I, or the window outside 1..J
+    const bool edge = r0 - H - 1 < 1 || r0 + kWfR + H > G.I || wc0 < 1 || wc0 + 128 > G.J + 1;
+    if (edge)
+        wf_warp<H, WIDE, true, PH2>(G, r0, wc0);
+    else
+        wf_warp<H, WIDE, false, PH2>(G, r0, wc0);
+}
+
+template <int H, bool WIDE>
+void launch_wavefront_w(const WfGeom &G, bool ph2, const int *flag, int mode, unsigned blocks, cudaStream_t st) {
+    if (ph2)
+        k_jacobi2d_wavefront<H, WIDE, true><<<blocks, kWfWarps * 32, 0, st>>>(G, flag, mode);
+    else
+        k_jacobi2d_wavefront<H, WIDE, false><<<blocks, kWfWarps * 32, 0, st>>>(G, flag, mode);
+}
+
+template <int H>
+int launch_wavefront(const WfGeom &G, bool ph2, const int *flag, int mode, cudaStream_t st) {
+    const int64_t warps = G.nbands * G.nwin;
+    const int64_t blocks = ceil_div(warps, kWfWarps);
+    if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "jacobi2d temporal: grid too large");
+    if (mode != 0) launch_wavefront_w<H, false>(G, ph2, flag, mode, (unsigned)blocks, st);  // narrow (or flag)
+    if (mode != 1) launch_wavefront_w<H, true>(G, ph2, flag, mode, (unsigned)blocks, st);   // wide (or flag)
+    return after_launch("jacobi2d_wavefront");
+}
+
 }  // namespace
 
 // h-step pass starting at step t0 (h odd, 3 <= h <= 11) over rows [lo, hi)
@@ -217,6 +406,34 @@ int jacobi2d_temporal_pass(const pk_launch_t &L, int *a, int64_t lo, int64_t hi,
     int *half0 = a, *half1 = a + L.N * L.N;
     const int *src = (t0 % 2 == 0) ? half0 : half1;       // s(t0): t even reads half 0
     int *dst = ((t0 + h - 1) % 2 == 0) ? half1 : half0;   // d(t0 + h - 1)
+    if (!(L.flags & PK_FLAG_GENERIC) && (L.N % 2) == 0 && aligned16(a)) {
+        WfGeom W;
+        W.src = src;
+        W.dst = dst;
+        W.half0 = half0;
+        W.half1 = half1;
+        W.N = L.N;
+        W.I = I;
+        W.J = J;
+        W.lo = lo;
+        W.hi = hi;
+        W.t0 = t0;
+        W.rs = (lo & 1) ? lo : lo - 1;  // bands start on odd rows (r0 - h even)
+        W.nbands = ceil_div(hi - W.rs, kWfR);
+        const int H4 = (h + 3) & ~3;
+        W.TJ = 128 - 2 * H4;
+        W.nwin = ceil_div(J + 1, W.TJ);  // output columns 0 .. J
+        const bool ph2 = (L.N & 3) == 2;
+        switch (h) {
+            case 1: return launch_wavefront<1>(W, ph2, flag, mode, st);
+            case 3: return launch_wavefront<3>(W, ph2, flag, mode, st);
+            case 5: return launch_wavefront<5>(W, ph2, flag, mode, st);
+            case 7: return launch_wavefront<7>(W, ph2, flag, mode, st);
+            case 9: return launch_wavefront<9>(W, ph2, flag, mode, st);
+            case 11: return launch_wavefront<11>(W, ph2, flag, mode, st);
+            default: break;
+        }
+    }
     T2Geom G;
     G.N = L.N;
     G.I = I;
