@@ -94,3 +94,19 @@ def test_temporal_jacobi1d_full_size_matches_per_step(cuda):
     want = run_program(programs.source("jacobi"), params, {"a": a})["a"]
     got = run_program(programs.source("jacobi"), params, {"a": a}, temporal=15)["a"]
     assert torch.equal(got, want)
+
+
+def test_temporal_jacobi2d_full_size_matches_per_step(cuda):
+    """N = 16386 (BASELINE configs[3]): the register-wavefront h = 7 passes and
+    the per-step sweeps leave identical double buffers (T = 17: two 7-step
+    passes, a 1-step remainder and the closing sweep)."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs, run_program
+
+    N = 16386
+    params = {"T": 17, "N": N, "s": 32, "B0": 64, "B1": 4}
+    g = torch.Generator(device="cuda").manual_seed(98)
+    a = torch.randint(-(1 << 20), 1 << 20, (2 * N, N), dtype=torch.int32, device="cuda", generator=g)
+    want = run_program(programs.source("jacobi2d"), params, {"a": a})["a"]
+    got = run_program(programs.source("jacobi2d"), params, {"a": a}, temporal=7)["a"]
+    assert torch.equal(got, want)
