@@ -27,11 +27,19 @@
 namespace pk {
 namespace {
 
-constexpr int TM = 128, TN = 256, TK = 32;       // output tile and K slab (32 fp32 = one 128B swizzle row)
-constexpr int A_BYTES = TM * TK * 4;             // 16 KB
-constexpr int B_BYTES = TN * TK * 4;             // 32 KB
+#ifndef PK_TF32_TK
+#define PK_TF32_TK 32
+#endif
+// K slab: 32 fp32 = one 128-byte swizzle row, 2 stages of 96 KB.  (16-wide
+// slabs with 64-byte swizzle and 4 stages of 48 KB compile too,
+// -DPK_TF32_TK=16: 5.38 ms at n = 8192 against 4.73 -- the ring depth is not
+// what limits this kernel.)
+constexpr int TM = 128, TN = 256, TK = PK_TF32_TK;
+constexpr int A_BYTES = TM * TK * 4;
+constexpr int B_BYTES = TN * TK * 4;
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int STAGES = 2;
+constexpr int STAGES = TK == 32 ? 2 : 4;
+constexpr int SWZ_BYTES = TK * 4;                // swizzle span = one slab row (64 or 128 B)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t TMEM_COLS = 256;
 
@@ -81,11 +89,13 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-// K-major, 128-byte swizzle UMMA shared-memory descriptor (rows of 128 B,
-// 8-row atoms of 1024 B stacked contiguously: SBO = 1024 B; LBO unused).
+// K-major swizzled UMMA shared-memory descriptor: rows of SWZ_BYTES, 8-row
+// atoms stacked contiguously (SBO = 8 rows), LBO unused; layout type 2 =
+// 128-byte swizzle, 4 = 64-byte swizzle (sm_100 descriptor encoding).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void *p) {
     const uint64_t addr = smem_u32(p);
-    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+    constexpr uint64_t sbo = (8 * SWZ_BYTES) >> 4, layout = SWZ_BYTES == 128 ? 2 : 4;
+    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (sbo << 32) | (1ull << 46) | (layout << 61);
 }
 
 // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M x N
@@ -249,7 +259,8 @@ int make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t K, int box
     cuuint32_t box[2] = {(cuuint32_t)TK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, SWZ_BYTES == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return PK_OK;

@@ -297,8 +297,13 @@ class PeerStencil:
         and raise if a wait gave up."""
         torch, dist = self._torch, self._dist
         torch.cuda.synchronize(self.a.device)
-        dist.barrier(group=self.group)
-        if int(self.ctr[2].item()) != 0:
+        # every rank learns whether any wait gave up, so all of them raise together
+        # (one rank raising alone would leave the others in the next collective)
+        err = torch.tensor([int(self.ctr[2].item())], dtype=torch.int64)
+        if dist.get_backend(self.group) == "nccl":
+            err = err.to(self.a.device)
+        dist.all_reduce(err, op=dist.ReduceOp.MAX, group=self.group)
+        if int(err.item()) != 0:
             raise RuntimeError("PeerStencil: a neighbour never signalled (wait timed out)")
 
     def close(self) -> None:
