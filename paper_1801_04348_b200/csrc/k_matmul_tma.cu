@@ -91,7 +91,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
     // grouped raster: blocks launched together cover a GROUP x (all columns)
     // band walked column-group by column-group, so the a rows and b columns
     // a wave touches stay resident in L2
-    constexpr int GROUP = 8;
+#ifndef PK_MM_GROUP
+#define PK_MM_GROUP 8
+#endif
+    constexpr int GROUP = PK_MM_GROUP;
     const int ntm = (int)(gridDim.x / ntn);
     const int per_group = GROUP * ntn;
     const int g = blockIdx.x / per_group, first = g * GROUP;
