@@ -20,6 +20,12 @@
 //   and the wider slab halves the barrier round trips per FLOP.
 #include <cuda.h>
 
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 #include "pk_internal.cuh"
 
 namespace pk {
@@ -77,77 +83,66 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
-                                                          const __grid_constant__ CUtensorMap map_b,
-                                                          float *__restrict__ C, int64_t ldc, int64_t rlo,
-                                                          int ntn, int ktiles) {
-    extern __shared__ unsigned char smem_raw[];
-    // align by offsetting the shared array itself (not via an integer cast), so
-    // the compiler keeps the shared address space and emits LDS, not generic LD
-    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-    uint64_t *empty = full + STAGES;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    // grouped raster: blocks launched together cover a GROUP x (all columns)
-    // band walked column-group by column-group, so the a rows and b columns
-    // a wave touches stay resident in L2
 #ifndef PK_MM_GROUP
 #define PK_MM_GROUP 8
 #endif
+
+// Tile t of the grouped raster: tiles launched together cover a GROUP x
+// (all columns) band walked column-group by column-group, so the a rows and
+// b columns a wave touches stay resident in L2.
+__device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int &m0, int &n0) {
     constexpr int GROUP = PK_MM_GROUP;
-    const int ntm = (int)(gridDim.x / ntn);
     const int per_group = GROUP * ntn;
-    const int g = blockIdx.x / per_group, first = g * GROUP;
+    const int g = t / per_group, first = g * GROUP;
     const int gsize = min(ntm - first, GROUP);
-    const int local = blockIdx.x - g * per_group;
-    const int tm = first + local % gsize, tn = local / gsize;
-    const int m0 = tm * BM, n0 = tn * BN;  // m0 relative to this launch's first row
+    const int local = t - g * per_group;
+    m0 = (first + local % gsize) * BM;
+    n0 = (local / gsize) * BN;
+}
 
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCOMP / 32);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    // thread 0 doubles as the TMA producer: at step kt it refills the stage of
-    // slab kt + AHEAD once every warp has released that stage's previous slab
-    auto produce = [&](int kt) {
-        const int s = kt % STAGES;
-        mbar_wait(&empty[s], ((kt / STAGES) & 1) ^ 1);
+// Slabs [kb, ke) of tile (m0, n0): c rows -> packed accumulators, the ring,
+// accumulators -> c.  gs: this CTA's running slab count (the ring's stage and
+// barrier phase continue across work items).
+__device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtensorMap *map_b, float *__restrict__ C,
+                                        int64_t ldc, int64_t rlo, int m0, int n0, int kb, int ke, int &gs,
+                                        unsigned char *smem, uint64_t *full, uint64_t *empty) {
+    const int tid = threadIdx.x;
+    const int nk = ke - kb;
+    // thread 0 doubles as the TMA producer: for slab j it refills the stage of
+    // slab j + AHEAD once every warp has released that stage's previous slab
+    auto produce = [&](int j) {
+        const int g = gs + j, s = g % STAGES;
+        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
         // the consumers read the stage through the generic proxy (LDS); order
         // those reads before the async-proxy (TMA) overwrite -- without this
         // fence n = 8192 runs lost a k-slab of one tile every few launches
         fence_proxy_async();
         unsigned char *st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(st, &map_at, &full[s], m0, kt * BK);
-        tma_load_2d(st + A_SLAB, &map_b, &full[s], n0, kt * BK);
+        tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);
+        tma_load_2d(st + A_SLAB, map_b, &full[s], n0, (kb + j) * BK);
     };
     if (tid == 0)
-        for (int kt = 0; kt < AHEAD && kt < ktiles; kt++) produce(kt);
-    (void)warp;
+        for (int j = 0; j < AHEAD && j < nk; j++) produce(j);
 
-    // ---- compute (all 8 warps)
     const int tx = tid % TX, ty = tid / TX;
     float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
     const int64_t chalf = (int64_t)(BM / 2) * ldc;
     // accumulators as packed column pairs: acc[i][jp] = {c[i][2jp], c[i][2jp+1]}
-    // (the operand format of fma.rn.f32x2, so the loop never repacks them)
+    // (the operand format of fma.rn.f32x2, so the loop never repacks them).
+    // c through L2 (.cg): a tile's earlier slabs may have been run by another SM
     unsigned long long acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; i++) {
         const float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
-        const ulonglong2 l = *reinterpret_cast<const ulonglong2 *>(cr);
-        const ulonglong2 h = *reinterpret_cast<const ulonglong2 *>(cr + BN / 2);
+        const ulonglong2 l = __ldcg(reinterpret_cast<const ulonglong2 *>(cr));
+        const ulonglong2 h = __ldcg(reinterpret_cast<const ulonglong2 *>(cr + BN / 2));
         acc[i][0] = l.x; acc[i][1] = l.y; acc[i][2] = h.x; acc[i][3] = h.y;
     }
-    for (int kt = 0; kt < ktiles; kt++) {
-        const int s = kt % STAGES;
-        if (tid == 0 && kt + AHEAD < ktiles) produce(kt + AHEAD);
-        mbar_wait(&full[s], (kt / STAGES) & 1);
+    for (int j = 0; j < nk; j++) {
+        const int g = gs + j, s = g % STAGES;
+        if (tid == 0 && j + AHEAD < nk) produce(j + AHEAD);
+        mbar_wait(&full[s], (g / STAGES) & 1);
         const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
 #pragma unroll
@@ -168,11 +163,82 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
+    gs += nk;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
         float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
         *reinterpret_cast<ulonglong2 *>(cr) = make_ulonglong2(acc[i][0], acc[i][1]);
         *reinterpret_cast<ulonglong2 *>(cr + BN / 2) = make_ulonglong2(acc[i][2], acc[i][3]);
+    }
+}
+
+__device__ __forceinline__ void mm_init(unsigned char *&smem, uint64_t *&full, uint64_t *&empty,
+                                        unsigned char *smem_raw) {
+    // align by offsetting the shared array itself (not via an integer cast), so
+    // the compiler keeps the shared address space and emits LDS, not generic LD
+    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    empty = full + STAGES;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCOMP / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+// One 128 x 128 tile per CTA, the whole reduction.
+__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
+                                                          const __grid_constant__ CUtensorMap map_b,
+                                                          float *__restrict__ C, int64_t ldc, int64_t rlo,
+                                                          int ntn, int ktiles) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem;
+    uint64_t *full, *empty;
+    mm_init(smem, full, empty, smem_raw);
+    int m0, n0, gs = 0;
+    tile_origin(blockIdx.x, (int)(gridDim.x / ntn), ntn, m0, n0);
+    mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
+}
+
+// Persistent CTAs over an order-preserving split of the work (see
+// mm_schedule): CTA p runs its items in order; an item that continues a
+// tile's reduction waits until the part before it has stored c (the tile's
+// progress word equals its first slab), and every item publishes its last
+// slab after storing.  c is the fp32 accumulator between the parts, so the
+// bits equal one launch.  Items: {tile, first slab, end slab}; CTA p owns
+// items [off[p], off[p+1]).
+__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_constant__ CUtensorMap map_at,
+                                                                const __grid_constant__ CUtensorMap map_b,
+                                                                float *__restrict__ C, int64_t ldc, int64_t rlo,
+                                                                int ntm, int ntn, const int3 *__restrict__ items,
+                                                                const int *__restrict__ off, int *progress) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem;
+    uint64_t *full, *empty;
+    mm_init(smem, full, empty, smem_raw);
+    int gs = 0;
+    for (int it = off[blockIdx.x]; it < off[blockIdx.x + 1]; it++) {
+        const int3 w = items[it];
+        int m0, n0;
+        tile_origin(w.x, ntm, ntn, m0, n0);
+        if (w.y > 0) {  // the tile's slabs before w.y are another CTA's: wait for their c
+            if (threadIdx.x == 0) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(progress + w.x) : "memory");
+                } while (v != w.y);
+            }
+            __syncthreads();
+        }
+        mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, w.y, w.z, gs, smem, full, empty);
+        __syncthreads();  // every thread's c stores before the publication
+        if (threadIdx.x == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(progress + w.x), "r"(w.z) : "memory");
+        }
     }
 }
 
@@ -217,6 +283,72 @@ bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc,
            n % 4 == 0 && n <= ((int64_t)1 << 30);
 }
 
+namespace {
+
+// Order-preserving split of the work over P persistent CTAs (the tail fix).
+// The T tiles x KS slabs are laid end to end and cut into P equal runs, so
+// every CTA gets T*KS/P slabs instead of whole tiles (T/P waves: 13.84 at
+// n = 8192 on one B200, 1.73 per rank at 8 ranks -- the last wave 73 % full).
+// A run covers [tail of tile A] [full tiles] [head of tile B]; the CTA runs
+// the head of B first, then the full tiles, then the tail of A, so the part
+// of a split tile that comes first in k runs at the start of one CTA's
+// timeline and the part after it at the end of the next CTA's (a tile is
+// shorter than a run, so the wait is normally already satisfied).  Waits
+// only go to lower-numbered CTAs, whose first item is the awaited one.
+struct DevSched {
+    int3 *items = nullptr;
+    int *off = nullptr;
+};
+
+std::mutex g_sched_mu;
+std::map<std::tuple<int, int64_t, int64_t, int>, DevSched> g_sched;  // (device, T, KS, P)
+
+int build_schedule(int64_t T, int64_t KS, int P, std::vector<int3> &items, std::vector<int> &off) {
+    const int64_t S = T * KS;
+    off.assign(P + 1, 0);
+    for (int p = 0; p < P; p++) {
+        const int64_t s0 = S * p / P, s1 = S * (p + 1) / P;
+        off[p] = (int)items.size();
+        if (s1 <= s0) continue;
+        const int64_t t0 = s0 / KS, t1 = (s1 - 1) / KS;
+        if (t0 == t1) {  // inside one tile
+            items.push_back(make_int3((int)t0, (int)(s0 - t0 * KS), (int)(s1 - t0 * KS)));
+            continue;
+        }
+        const int64_t k0 = s0 - t0 * KS, k1 = s1 - t1 * KS;  // first piece from k0, last piece up to k1
+        if (k1 < KS) items.push_back(make_int3((int)t1, 0, (int)k1));                 // head of the next split
+        for (int64_t t = k0 == 0 ? t0 : t0 + 1; t <= (k1 == KS ? t1 : t1 - 1); t++)  // whole tiles
+            items.push_back(make_int3((int)t, 0, (int)KS));
+        if (k0 > 0) items.push_back(make_int3((int)t0, (int)k0, (int)KS));            // tail of the previous
+    }
+    off[P] = (int)items.size();
+    return PK_OK;
+}
+
+int schedule_for(int dev, int64_t T, int64_t KS, int P, DevSched *out) {
+    std::lock_guard<std::mutex> lock(g_sched_mu);
+    const auto key = std::make_tuple(dev, T, KS, P);
+    auto it = g_sched.find(key);
+    if (it != g_sched.end()) {
+        *out = it->second;
+        return PK_OK;
+    }
+    std::vector<int3> items;
+    std::vector<int> off;
+    build_schedule(T, KS, P, items, off);
+    DevSched d;
+    cudaError_t e = cudaMalloc(&d.items, items.size() * sizeof(int3));
+    if (e == cudaSuccess) e = cudaMalloc(&d.off, off.size() * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemcpy(d.items, items.data(), items.size() * sizeof(int3), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul schedule: %s", cudaGetErrorString(e));
+    g_sched[key] = d;
+    *out = d;
+    return PK_OK;
+}
+
+}  // namespace
+
 int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
                       int64_t K, cudaStream_t st) {
     const int64_t rows = rhi - rlo;
@@ -229,11 +361,36 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
         CUtensorMap mat, mb;
         if ((rc = make_map(&mat, at, K, rows, rows, BM, BK)) == PK_OK &&
             (rc = make_map(&mb, b, K, Nc, n, BN, BK)) == PK_OK &&
-            (rc = allow_smem((const void *)k_matmul_tma, SMEM_BYTES)) == PK_OK) {
-            const int ntn = (int)(Nc / BN);
-            k_matmul_tma<<<(unsigned)((rows / BM) * ntn), NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn,
-                                                                                       (int)(K / BK));
-            rc = after_launch("matmul_tma");
+            (rc = allow_smem((const void *)k_matmul_tma, SMEM_BYTES)) == PK_OK &&
+            (rc = allow_smem((const void *)k_matmul_tma_sched, SMEM_BYTES)) == PK_OK) {
+            const int ntn = (int)(Nc / BN), ntm = (int)(rows / BM);
+            const int64_t T = (int64_t)ntm * ntn, KS = K / BK;
+            // persistent split when the tiles leave the last wave part-empty
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matmul_tma_sched, NTHREADS, SMEM_BYTES);
+            const int64_t P = (int64_t)sms * per_sm;
+            const bool split = getenv("PK_MM_NO_SPLIT") == nullptr && P > 0 && T > P && T % P != 0 && KS >= 8 &&
+                               T * KS < ((int64_t)1 << 31);
+            if (split) {
+                DevSched d;
+                int *progress = nullptr;
+                if ((rc = schedule_for(dev, T, KS, (int)P, &d)) == PK_OK) {
+                    e = scratch_alloc((void **)&progress, (size_t)T * sizeof(int), st);
+                    if (e != cudaSuccess) rc = fail(PK_E_ALLOC, "matmul progress words: %s", cudaGetErrorString(e));
+                }
+                if (rc == PK_OK) {
+                    cudaMemsetAsync(progress, 0, (size_t)T * sizeof(int), st);
+                    k_matmul_tma_sched<<<(unsigned)P, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntm, ntn,
+                                                                                  d.items, d.off, progress);
+                    rc = after_launch("matmul_tma_sched");
+                    cudaFreeAsync(progress, st);
+                }
+            } else {
+                k_matmul_tma<<<(unsigned)T, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn, (int)KS);
+                rc = after_launch("matmul_tma");
+            }
         }
     }
     cudaFreeAsync(at, st);
