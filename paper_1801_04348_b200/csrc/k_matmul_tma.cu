@@ -286,15 +286,16 @@ bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc,
 namespace {
 
 // Order-preserving split of the work over P persistent CTAs (the tail fix).
-// The T tiles x KS slabs are laid end to end and cut into P equal runs, so
-// every CTA gets T*KS/P slabs instead of whole tiles (T/P waves: 13.84 at
-// n = 8192 on one B200, 1.73 per rank at 8 ranks -- the last wave 73 % full).
-// A run covers [tail of tile A] [full tiles] [head of tile B]; the CTA runs
-// the head of B first, then the full tiles, then the tail of A, so the part
-// of a split tile that comes first in k runs at the start of one CTA's
-// timeline and the part after it at the end of the next CTA's (a tile is
-// shorter than a run, so the wait is normally already satisfied).  Waits
-// only go to lower-numbered CTAs, whose first item is the awaited one.
+// The last 1-2 waves of tiles x KS slabs are laid end to end and cut into P
+// equal runs, so every CTA gets the same number of slabs instead of whole
+// tiles (T/P waves: 13.84 at n = 8192 on one B200, 1.73 per rank at 8
+// ranks -- the last wave 73 % full).  A run covers [tail of tile A] [full
+// tiles] [head of tile B]; the CTA runs the head of B first, then the full
+// tiles, then the tail of A, so the part of a split tile that comes first in
+// k runs at the start of one CTA's split phase and the part after it at the
+// end of the next CTA's (a run is at least one tile long, so the wait is
+// already satisfied).  Waits only go to lower-numbered CTAs, whose head item
+// is the awaited one and follows only unconditional whole tiles.
 struct DevSched {
     int3 *items = nullptr;
     int *off = nullptr;
@@ -304,22 +305,28 @@ std::mutex g_sched_mu;
 std::map<std::tuple<int, int64_t, int64_t, int>, DevSched> g_sched;  // (device, T, KS, P)
 
 int build_schedule(int64_t T, int64_t KS, int P, std::vector<int3> &items, std::vector<int> &off) {
-    const int64_t S = T * KS;
+    // all but the last 1-2 waves as whole tiles in raster order (CTA p takes
+    // tile w*P + p at step w, the tiles running together stay L2 neighbours),
+    // the rest split into equal runs of >= one tile (so a tile is cut at most
+    // once and its second part never waits in practice)
+    const int64_t W0 = T / P >= 2 ? T / P - 1 : 0;
+    const int64_t base = W0 * P, S = (T - base) * KS;
     off.assign(P + 1, 0);
     for (int p = 0; p < P; p++) {
-        const int64_t s0 = S * p / P, s1 = S * (p + 1) / P;
         off[p] = (int)items.size();
+        for (int64_t w = 0; w < W0; w++) items.push_back(make_int3((int)(w * P + p), 0, (int)KS));
+        const int64_t s0 = S * p / P, s1 = S * (p + 1) / P;
         if (s1 <= s0) continue;
         const int64_t t0 = s0 / KS, t1 = (s1 - 1) / KS;
         if (t0 == t1) {  // inside one tile
-            items.push_back(make_int3((int)t0, (int)(s0 - t0 * KS), (int)(s1 - t0 * KS)));
+            items.push_back(make_int3((int)(base + t0), (int)(s0 - t0 * KS), (int)(s1 - t0 * KS)));
             continue;
         }
         const int64_t k0 = s0 - t0 * KS, k1 = s1 - t1 * KS;  // first piece from k0, last piece up to k1
-        if (k1 < KS) items.push_back(make_int3((int)t1, 0, (int)k1));                 // head of the next split
-        for (int64_t t = k0 == 0 ? t0 : t0 + 1; t <= (k1 == KS ? t1 : t1 - 1); t++)  // whole tiles
-            items.push_back(make_int3((int)t, 0, (int)KS));
-        if (k0 > 0) items.push_back(make_int3((int)t0, (int)k0, (int)KS));            // tail of the previous
+        if (k1 < KS) items.push_back(make_int3((int)(base + t1), 0, (int)k1));          // head of the next split
+        for (int64_t t = k0 == 0 ? t0 : t0 + 1; t <= (k1 == KS ? t1 : t1 - 1); t++)    // whole tiles
+            items.push_back(make_int3((int)(base + t), 0, (int)KS));
+        if (k0 > 0) items.push_back(make_int3((int)(base + t0), (int)k0, (int)KS));     // tail of the previous
     }
     off[P] = (int)items.size();
     return PK_OK;
