@@ -314,12 +314,64 @@ def _deep_copy(v):
 
 
 def run_block(program, params, grid_values, context_values=None, arrays=None, tracer=None):
-    """The reference's one-block executor (interp.py:228-249) exists to feed
-    the footprint oracle's access tracer; it has no GPU counterpart."""
-    raise NotImplementedError(
-        "run_block is a CPU tracing aid of the reference interpreter (interp.py:228-249); "
-        "the GPU executor only runs whole programs"
-    )
+    """One thread block (interp.py:228-249): the grid indices fixed to
+    ``grid_values``, the serial context loop variables to ``context_values``,
+    the thread loops swept.  Runs the reference emitter's leaf for the
+    program (the original program, or its caching-off case program) with its
+    grid loops pinned, as a single block on the GPU (jit.run_block_leaf).
+    Returns every declared array like run_program; int programs only (the
+    emitted leaves compute on C ints)."""
+    global _last
+    if tracer is not None:
+        raise NotImplementedError(
+            "tracer is CPU-only instrumentation of the reference interpreter; "
+            "the GPU executor cannot report per-access events"
+        )
+    from . import jit
+
+    kind = identify(program)
+    if kind.is_original:
+        variant = "original"
+    elif tuple(kind.applied) == ("caching-off",):
+        variant = "caching-off"
+    else:
+        raise NotImplementedError("run_block runs the original program or its caching-off case program, "
+                                  "not %s" % (kind.applied,))
+    fam = FAMILIES[kind.family]
+    arrays = dict(arrays or {})
+    if any(_dtype_of(v) == "f" for n, v in arrays.items() if n in {a.name for a in fam.arrays}):
+        raise NotImplementedError("run_block computes on C ints (the emitted leaves are int kernels)")
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("run_block needs a CUDA device (sm_100a); there is no CPU fallback")
+    leaf = jit.packaged_leaf(kind.family, variant)
+    P = effective_params(kind, params)
+    shapes = _shapes_py(fam, P)
+    kinds = [_kind_of(v) for v in arrays.values()]
+    default_kind = kinds[0] if kinds else "list"
+    dev = torch.device("cuda", torch.cuda.current_device())
+    bufs, sizes = {}, {}
+    for a in fam.arrays:
+        shape = shapes[a.name]
+        if a.name in arrays:
+            bufs[a.name], sizes[a.name] = _to_device_tensor(a.name, arrays[a.name], shape, np.int32, dev)
+        else:
+            bufs[a.name] = torch.zeros(max(_numel(shape), 1), dtype=torch.int32, device=dev)
+            sizes[a.name] = _numel(shape)
+    jit.run_block_leaf(leaf, P, dict(grid_values), dict(context_values or {}), bufs,
+                       torch.cuda.current_stream(dev).cuda_stream)
+    torch.cuda.current_stream(dev).synchronize()
+    _last = RunInfo(kind.family, None, tuple(kind.applied), False, {"kernel": leaf.kernel_name, "block": True}, 0)
+    out = {}
+    for name, v in arrays.items():
+        if name not in bufs:
+            out[name] = _deep_copy(v)
+    for a in fam.arrays:
+        shape = shapes[a.name]
+        like = arrays.get(a.name)
+        k = _kind_of(like) if like is not None else default_kind
+        out[a.name] = _from_device(bufs[a.name][: _numel(shape)], k, shape, like)
+    return out
 
 
 def c_div(a: int, b: int) -> int:

@@ -263,6 +263,88 @@ def run_leaf(leaf: Leaf, params: dict, buffers: dict, stream: int = 0) -> int:
     return count
 
 
+# -------------------------------------------------------------- run_block --
+
+_packaged: dict = {}
+
+
+def packaged_leaf(family: str, variant: str) -> Leaf:
+    """The reference emitter's leaf for a family's original program or its
+    caching-off case program (data/leaves.json, tools/export_leaves.py)."""
+    import json
+    import os
+
+    if not _packaged:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "leaves.json")
+        with open(path) as fh:
+            _packaged.update(json.load(fh)["leaves"])
+    key = "%s/%s" % (family, variant)
+    if key not in _packaged:
+        raise NotImplementedError("no emitted leaf for %s (%s)" % (family, variant))
+    return Leaf.from_json(_packaged[key])
+
+
+_GRID_LOOP = re.compile(r"for \(int (\w+) = \(int\)blockIdx\.[xyz]; \1 < [^;]+; \1 \+= PK_GRID_STRIDE\)")
+
+
+def block_leaf(leaf: Leaf) -> Leaf:
+    """The same kernel with every grid meta_for pinned to one value (a kernel
+    argument pk_rb_<var>): launched as one block it runs exactly the body
+    instances interp.run_block sweeps (grid indices fixed, thread loops over
+    the block's threads, interp.py:228-249)."""
+    vars_ = [v for v, _ in leaf.grid]
+    src, n = _GRID_LOOP.subn(lambda m: "for (int {0} = pk_rb_{0}, pk_once_{0} = 1; pk_once_{0}; pk_once_{0} = 0)"
+                             .format(m.group(1)), leaf.source)
+    if n != len(vars_):
+        raise NotImplementedError("emitted grid loops of %s not in the expected form" % leaf.kernel_name)
+    sig = re.search(r"(__global__ void %s\()([^)]*)\)" % re.escape(leaf.kernel_name), src)
+    src = src[:sig.end(2)] + "".join(", int pk_rb_%s" % v for v in vars_) + src[sig.end(2):]
+    b = Leaf(**{k: getattr(leaf, k) for k in Leaf.__dataclass_fields__})
+    b.source = src
+    b.args = list(leaf.args) + [("pk_rb_%s" % v, "int") for v in vars_]
+    return b
+
+
+def run_block_leaf(leaf: Leaf, params: dict, grid_values: dict, context_values: dict, buffers: dict,
+                   stream: int = 0) -> None:
+    """One block of an emitted leaf (see block_leaf) on device buffers."""
+    env = {p: int(params[p]) for p in leaf.params if p in params}
+    missing = [p for p in leaf.params if p not in params]
+    if missing:
+        raise KeyError("no value supplied for parameter %r" % missing[0])
+    for b, expr in leaf.bindings:
+        env[b] = ceval(expr, env)
+    roles = [(v, b, grid_values) for v, b in leaf.grid] + [(v, b, context_values) for v, b in leaf.context]
+    for var, bound, src in roles:
+        if var not in src:
+            raise KeyError("no value supplied for %r" % var)
+        v, hi = int(src[var]), ceval(bound, env)
+        # outside its loop's range the reference runs the body anyway and
+        # raises IndexError only if an access leaves its array; here such a
+        # block is refused before it runs
+        if not 0 <= v < hi:
+            raise IndexError("%s = %d outside its loop range [0, %d)" % (var, v, hi))
+        env[var] = v
+    block = [max(0, ceval(e, env)) for _, e in leaf.thread]
+    if any(x == 0 for x in block):
+        return  # an empty thread meta_for: nothing runs
+    if eval_product(block) > 1024:
+        raise ValueError("thread block of %d threads exceeds T_B = 1024" % eval_product(block))
+    bl = block_leaf(leaf)
+    h = compile_leaf(bl, env)
+    for var, _ in leaf.grid:
+        env["pk_rb_" + var] = env[var]
+    vals, kinds = [], []
+    for name, kind in bl.args:
+        if kind == "ptr":
+            vals.append(buffers[name].data_ptr())
+            kinds.append(1)
+        else:
+            vals.append(env[name])
+            kinds.append(0)
+    _lib.jit_launch(h, [1] * len(leaf.grid), list(reversed(block)), vals, kinds, 0, stream)
+
+
 def eval_product(xs) -> int:
     p = 1
     for x in xs:

@@ -145,6 +145,16 @@ def registry() -> dict[str, ProgramKind]:
             applied = tuple(s for s in case["applied"] if s in SOURCE_STRATEGIES)
             key = normalize(case["program"])
             reg.setdefault(key, ProgramKind(fam, applied, tuple(case["params"]), case["program"]))
+    # the original programs with caching-off alone (the reference's
+    # strategies.apply_source; not a leaf of any case tree, but a program a
+    # caller may run): bound to the direct kernels
+    leaves = os.path.join(DATA, "leaves.json")
+    if os.path.exists(leaves):
+        with open(leaves) as fh:
+            for name, p in json.load(fh).get("programs", {}).items():
+                fam = name.split("/")[0]
+                params = FAMILIES[fam].params if fam in FAMILIES else tuple(p["params"])
+                reg.setdefault(normalize(p["text"]), ProgramKind(fam, ("caching-off",), params, p["text"]))
     return reg
 
 

@@ -56,3 +56,22 @@ def test_emitted_leaves_match_reference_on_gpu(cuda):
                 assert got[name] == want, (e["program"], e["variant"], v["params"], name)
             checked += 1
     assert checked >= 20
+
+
+def test_block_leaf_pins_every_grid_loop():
+    """run_block's kernel: each packaged leaf's grid meta_for loops become a
+    single iteration at a kernel argument (no GPU needed)."""
+    import re
+
+    from paper_1801_04348_b200 import jit
+
+    for fam in ("addition", "jacobi", "jacobi2d", "matmul", "matvec", "reverse", "transpose"):
+        for variant in ("original", "caching-off"):
+            if fam == "addition" and variant == "caching-off":
+                continue
+            leaf = jit.packaged_leaf(fam, variant)
+            b = jit.block_leaf(leaf)
+            assert "PK_GRID_STRIDE)" not in re.sub(r"#.*", "", b.source.split("__global__")[1])
+            for var, _ in leaf.grid:
+                assert "int pk_rb_%s" % var in b.source
+                assert ("pk_rb_%s" % var, "int") in b.args
