@@ -327,3 +327,29 @@ def test_matvec_full_size_exact(cuda):
     got = _run(programs.source("matvec"), {"N": N, "s": 1, "B": 256}, {"a": a, "x": x, "y": y})["y"]
     want = (y.double() + a.double() @ x.double()).int()
     assert torch.equal(got.reshape(-1), want)
+
+
+@pytest.mark.parametrize("rows", [(0, 640), (0, 1024), (1280, 2560), (4096, 8192)])
+def test_matmul_split_schedule_exact_on_row_shares(cuda, rows):
+    """Row shares whose tile count leaves a part-empty last wave take the
+    order-preserving persistent split (k_matmul_tma_sched: a cut tile's second
+    part waits for the first's c); integer-valued fp32 keeps every partial sum
+    exact, so the rows must equal a binary64 product and the other rows stay
+    untouched."""
+    torch = cuda
+    from paper_1801_04348_b200 import _lib, binding, programs
+
+    n = 8192
+    lo, hi = rows
+    g = torch.Generator(device="cuda").manual_seed(lo + hi)
+    a = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    b = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    c = torch.randint(-8, 9, (n, n), device="cuda", generator=g).float()
+    want = c[lo:hi].double() + a[lo:hi].double() @ b.double()
+    L = binding.make_launch(programs.original("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": 16}, (),
+                            _lib.DTYPE_F32, lo=lo, hi=hi)
+    got = c.clone()
+    _lib.launch(L, [a.data_ptr(), b.data_ptr(), got.data_ptr()], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(got[lo:hi].double(), want)
+    assert torch.equal(got[:lo], c[:lo]) and torch.equal(got[hi:], c[hi:])
