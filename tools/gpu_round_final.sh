@@ -13,15 +13,15 @@ cap() {  # name regex skip args...
       $P "$@" > $D/$name.log 2>&1
   echo "$name rc=$?"
 }
-cap matmul k_matmul_tma 1 matmul '{"n": 8192, "B0": 128, "ub1": 8, "s": 16}' 3
+cap matmul k_matmul_tma_sched 1 matmul '{"n": 8192, "B0": 128, "ub1": 8, "s": 16}' 3
 cap tf32x3 k_tf32x3 1 matmul '{"n": 8192, "B0": 128, "ub1": 8, "s": 16}' 3 --tf32x3
 cap jacobi1d k_jacobi1d_reg 3 jacobi '{"T": 4, "N": 268435458, "s": 16, "B": 256}' 1
 cap jacobi2d k_jacobi2d_reg 3 jacobi2d '{"T": 4, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1
 cap jacobi1d_tma k_jacobi1d_tma 3 jacobi '{"T": 4, "N": 268435458, "s": 16, "B": 256}' 1 --generic
 cap jacobi2d_tma k_jacobi2d_tma 3 jacobi2d '{"T": 4, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1 --generic
-cap jacobi2d_temporal k_jacobi2d_temporal 0 jacobi2d '{"T": 8, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1 --temporal=7
+cap jacobi2d_temporal k_jacobi2d_wavefront 0 jacobi2d '{"T": 8, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1 --temporal=7
 cap reverse k_reverse 1 reverse '{"N": 1073741824, "s": 16, "B": 256}' 3
 cap transpose k_transpose 1 transpose '{"N": 32768, "s": 8, "B0": 64, "B1": 8}' 3
 cap matvec k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 256}' 3
-cap temporal k_jacobi1d_temporal 0 jacobi '{"T": 16, "N": 268435458, "s": 16, "B": 256}' 1 --temporal=15
+cap temporal k_jacobi1d_rtemporal 0 jacobi '{"T": 16, "N": 268435458, "s": 16, "B": 256}' 1 --temporal=15
 ls -la $D
