@@ -258,6 +258,10 @@ class PeerStencil:
         self.family, self.P, self.a, self.L, self.group = family, P, a, launch, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.lo, self.hi = split(family, P, self.rank, self.world)
+        # every rank's edge blocks signal its neighbours each step: an empty
+        # slab would leave them waiting
+        if any(h <= l for l, h in (split(family, P, r, self.world) for r in range(self.world))):
+            raise ValueError("PeerStencil: %d ranks for %s leave a rank without units" % (self.world, family))
         # [from_left, from_right, error] in this rank's memory
         self.ctr = torch.zeros(3, dtype=torch.int32, device=a.device)
         mine = (_lib.ipc_export(a.data_ptr()), _lib.ipc_export(self.ctr.data_ptr()))
