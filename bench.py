@@ -479,6 +479,39 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
                             "because h steps share one HBM pass; results bit-identical"}
         del bufs
         torch.cuda.empty_cache()
+    # the other size of BASELINE configs[1]: FP32 matmul n = 2048, (B0, ub1, s) tuned inside the case
+    n2 = 2048
+    kind = programs.original("matmul")
+    base = {"n": n2, "B0": 128, "ub1": 8, "s": 16}
+    g = torch.Generator(device="cuda").manual_seed(0x1801)
+    bufs = [torch.rand(n2 * n2, device="cuda", generator=g) * 2 - 1 for _ in range(3)]
+    grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in ((128, 8, 16), (64, 8, 16), (64, 8, 8), (128, 8, 8))]
+    if no_tune:
+        tuned, trials = dict(base), []
+    else:
+        tuned, trials = autotune.autotune(kind, base, machine=mv, buffers=bufs, reps=5, grid=grid)
+    sel = cases.select(kind, tuned, mv)
+    L = binding.make_launch(kind, tuned, sel.applied, _lib.DTYPE_F32)
+    ptrs = [x.data_ptr() for x in bufs]
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(20):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    gf = 2.0 * n2 ** 3 / (ms * 1e-3) / 1e9
+    peak = mv.props.get("sm_count", 148) * 256 * peaks["sm_max_mhz"] * 1e6 / 1e9
+    out["matmul_n2048"] = {"params": tuned, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 4),
+                           "value": round(gf, 1), "unit": "GFLOP/s", "frac_of_fp32_peak": round(gf / peak, 4),
+                           "tuning_trials": len(trials),
+                           "note": "256 tiles of 128 x 128 on 296 resident CTA slots: 0.86 of one wave"}
+    del bufs
+    torch.cuda.empty_cache()
     return out
 
 
