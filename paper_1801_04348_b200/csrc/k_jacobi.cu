@@ -53,19 +53,36 @@ __device__ __forceinline__ int avg5(int a, int b, int c, int d, int e) {
 }
 
 // flag = 1 if every |v| <= bound over a[0, n), else 0 (flag preset non-zero).
+// a need only be 4-byte aligned: the words before its first 16-byte boundary
+// are checked one by one.
 __global__ void __launch_bounds__(256) k_range_flag(const int *__restrict__ a, int64_t n, int bound,
                                                    int *__restrict__ flag) {
     bool ok = true;
-    const int64_t n4 = n / 4;
-    const int4 *a4 = reinterpret_cast<const int4 *>(a);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t head = (int64_t)(((16u - (reinterpret_cast<uintptr_t>(a) & 15u)) & 15u) >> 2);
+    if (head > n) head = n;
+    const int64_t n4 = (n - head) / 4;
+    const int4 *a4 = reinterpret_cast<const int4 *>(a + head);
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t0; i < n4; i += stride) {
         const int4 v = ld_stream(a4 + i);
         ok &= (v.x >= -bound && v.x <= bound) & (v.y >= -bound && v.y <= bound) &
               (v.z >= -bound && v.z <= bound) & (v.w >= -bound && v.w <= bound);
     }
-    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        ok &= (a[i] >= -bound && a[i] <= bound);
+    if (t0 < head) ok &= (a[t0] >= -bound && a[t0] <= bound);
+    for (int64_t i = head + 4 * n4 + t0; i < n; i += stride) ok &= (a[i] >= -bound && a[i] <= bound);
+    if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
+}
+
+// the same over columns 0 and J+1 .. N-1 of rows 1 .. I of an N x N half
+__global__ void __launch_bounds__(256) k_range_cols(const int *__restrict__ h, int64_t N, int64_t I, int64_t J,
+                                                   int bound, int *__restrict__ flag) {
+    bool ok = true;
+    const int64_t w = N - J;  // column 0 plus columns J+1 .. N-1
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < I * w; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = 1 + e / w, k = e % w, j = k == 0 ? 0 : J + k;
+        const int v = h[i * N + j];
+        ok &= (v >= -bound && v <= bound);
+    }
     if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
 }
 
@@ -848,18 +865,61 @@ int sweep2d_impl(const pk_launch_t &L, const int *src, int *dst, int64_t lo, int
     return after_launch("jacobi2d");
 }
 
-// Device flag: non-zero when the whole double buffer is within the narrow bound.
-int range_flag(const int *a, int64_t n, int bound, int **flag, cudaStream_t st) {
+// Device flag: non-zero when the values a run can read are within the narrow
+// bound.  range_flag_begin allocates and presets it; range_check clears it
+// if some |v| in a[0, n) exceeds the bound.
+int range_flag_begin(int **flag, cudaStream_t st) {
     cudaError_t err = scratch_alloc((void **)flag, sizeof(int), st);
     if (err != cudaSuccess) return fail(PK_E_ALLOC, "cudaMallocAsync(flag): %s", cudaGetErrorString(err));
     // the flag starts non-zero (bytes 0x01); the check clears it with atomicAnd
     err = cudaMemsetAsync(*flag, 1, sizeof(int), st);
     if (err != cudaSuccess) return fail(PK_E_CUDA, "flag init: %s", cudaGetErrorString(err));
+    return PK_OK;
+}
+
+int range_check(const int *a, int64_t n, int bound, int *flag, cudaStream_t st) {
+    if (n <= 0) return PK_OK;
     int64_t blocks = ceil_div(n / 4 + 1, 256 * 8);
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    k_range_flag<<<(unsigned)blocks, 256, 0, st>>>(a, n, bound, *flag);
+    k_range_flag<<<(unsigned)blocks, 256, 0, st>>>(a, n, bound, flag);
     return after_launch("range_flag");
+}
+
+int range_flag(const int *a, int64_t n, int bound, int **flag, cudaStream_t st) {
+    int rc = range_flag_begin(flag, st);
+    return rc ? rc : range_check(a, n, bound, *flag, st);
+}
+
+// What a whole-program run can read: every value of the half step 0 reads,
+// and the points of the other half the program never writes (step 0
+// overwrites the rest before anything reads it).  Half the bytes of the
+// whole double buffer.
+int range_flag_program(const pk_launch_t &L, const int *a, int **flag, cudaStream_t st) {
+    int rc = range_flag_begin(flag, st);
+    if (rc) return rc;
+    if (L.family == PK_FAMILY_JACOBI1D) {
+        Extents1D e;
+        if ((rc = extents1d(L, &e))) return rc;
+        // step 0 reads the upper half and writes positions 1 .. P of the lower one
+        if ((rc = range_check(a + L.N, L.N, kBound3, *flag, st))) return rc;
+        if ((rc = range_check(a, 1, kBound3, *flag, st))) return rc;
+        return range_check(a + e.P + 1, L.N - e.P - 1, kBound3, *flag, st);
+    }
+    Extents2D e;
+    if ((rc = extents2d(L, &e))) return rc;
+    const int64_t N = L.N;
+    const int *h1 = a + N * N;  // step 0 reads half 0 and writes rows 1..I x cols 1..J of half 1
+    if ((rc = range_check(a, N * N, kBound5, *flag, st))) return rc;
+    if ((rc = range_check(h1, N, kBound5, *flag, st))) return rc;
+    if ((rc = range_check(h1 + (e.I + 1) * N, (N - 1 - e.I) * N, kBound5, *flag, st))) return rc;
+    if (e.I > 0 && N - e.J > 0) {
+        int64_t blocks = ceil_div(e.I * (N - e.J), 256 * 4);
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        k_range_cols<<<(unsigned)blocks, 256, 0, st>>>(h1, N, e.I, e.J, kBound5, *flag);
+        rc = after_launch("range_cols");
+    }
+    return rc;
 }
 
 }  // namespace
@@ -939,8 +999,8 @@ int launch_jacobi1d(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     unit_range(L, 1, e.P + 1, &lo, &hi);
     int *a = static_cast<int *>(p[0]);
     int *flag = nullptr;
-    if (!(L.flags & PK_FLAG_NARROW)) {
-        rc = range_flag(a, 2 * L.N, kBound3, &flag, st);
+    if (!(L.flags & PK_FLAG_NARROW)) {  // partitioned runs (L.hi > 0) check the whole double buffer
+        rc = L.hi > 0 ? range_flag(a, 2 * L.N, kBound3, &flag, st) : range_flag_program(L, a, &flag, st);
         if (rc) return rc;
     }
     const bool temporal = (L.flags & PK_FLAG_TEMPORAL) && L.hi <= 0;  // whole-program runs only
@@ -979,8 +1039,8 @@ int launch_jacobi2d(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     int *a = static_cast<int *>(p[0]);
     int *half1 = a + L.N * L.N;
     int *flag = nullptr;
-    if (!(L.flags & PK_FLAG_NARROW)) {
-        rc = range_flag(a, 2 * L.N * L.N, kBound5, &flag, st);
+    if (!(L.flags & PK_FLAG_NARROW)) {  // partitioned runs (L.hi > 0) check the whole double buffer
+        rc = L.hi > 0 ? range_flag(a, 2 * L.N * L.N, kBound5, &flag, st) : range_flag_program(L, a, &flag, st);
         if (rc) return rc;
     }
     const bool temporal = (L.flags & PK_FLAG_TEMPORAL) && L.hi <= 0;  // whole-program runs only

@@ -108,3 +108,40 @@ def test_jacobi2d_reg_misaligned_base_falls_back(cuda):
         b = b_buf[off:off + 2 * N * N].view(2 * N, N)
         _sweep(torch, _launch("jacobi2d", params, True, False), b[:N], b[N:], 1, I + 1)
         assert torch.equal(b[N:], want)
+
+
+@pytest.mark.parametrize("where", ["overwritten", "boundary"])
+def test_range_check_covers_what_the_program_reads(cuda, oracle_mod, where):
+    """The narrow (int32-sum) path is chosen from the values a run can read:
+    the half step 0 reads and the never-written points of the other half.
+    Huge values in points step 0 overwrites do not matter; huge values in a
+    never-written boundary point force the 64-bit sums -- both bit-exact."""
+    import numpy as np
+
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(12)
+    big = 2**31 - 1
+    N = 2002
+    p1 = {"T": 5, "N": N, "s": 4, "B": 50}
+    a = rng.integers(-(1 << 20), 1 << 20, size=2 * N).astype(np.int32)
+    if where == "overwritten":
+        a[1:N - 1] = big  # lower half, positions 1 .. P: written by step 0 before any read
+    else:
+        a[0] = big  # lower half, position 0: never written, read from step 1 on
+        a[N - 1] = -big
+    want = oracle_mod.run("jacobi", p1, {"a": a})["a"]
+    got = run_program(programs.source("jacobi"), p1, {"a": a})["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
+
+    M = 130
+    p2 = {"T": 4, "N": M, "s": 2, "B0": 8, "B1": 16}
+    b = rng.integers(-(1 << 20), 1 << 20, size=(2 * M, M)).astype(np.int32)
+    if where == "overwritten":
+        b[M + 1:M + 129, 1:129] = big  # half 1, rows 1..I x cols 1..J
+    else:
+        b[M + 5, M - 1] = big  # half 1, column N-1 (> J): never written
+        b[M + 7, 0] = -big
+    want = oracle_mod.run("jacobi2d", p2, {"a": b})["a"]
+    got = run_program(programs.source("jacobi2d"), p2, {"a": b})["a"]
+    assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1))
