@@ -22,6 +22,8 @@
 //      warps 0-3:     epilogue, tcgen05.ld 32x32b.x32 from TMEM, + c, store
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "pk_internal.cuh"
 
 namespace pk {
@@ -231,6 +233,157 @@ __global__ void __launch_bounds__(128, 1) k_tf32x3(const __grid_constant__ CUten
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// ---- the 2-CTA form (default): a CTA pair on one TPC computes a 256 x 256
+// tile with tcgen05.mma.cta_group::2 (M = 256: each CTA's 128 rows of A and
+// 128 of the 256 columns of B in its own shared memory, the accumulator rows
+// of each CTA in its own TMEM).  Per SM and slab the operand bytes drop from
+// 96 KB to 64 KB (B is split across the pair), so the ring holds 3 stages.
+// Protocol (CUTLASS's 2x1SM pipeline): both CTAs' producers load their
+// halves with the 2-SM TMA, which completes on the LEADER's full barrier
+// (peer bit cleared from the barrier address); the leader arms that barrier
+// for both halves' bytes; the leader's single MMA thread issues the MMAs and
+// commits to the empty barriers of both CTAs (multicast) -- each producer
+// refills its own stage -- and finally to both CTAs' done barriers.
+constexpr int P_BN = 128;                              // B columns per CTA of the pair
+constexpr int P_B_BYTES = P_BN * TK * 4;
+constexpr int P_STAGE_BYTES = 2 * A_BYTES + 2 * P_B_BYTES;
+constexpr int P_STAGES = 3;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;         // shared::cluster address -> CTA 0 of the pair
+
+__device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    k_tf32x3_pair(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                  const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                  float *__restrict__ c, int64_t ldc, int ntn, int kslabs) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + P_STAGES * P_STAGE_BYTES);
+    uint64_t *empty = full + P_STAGES;
+    uint64_t *done = empty + P_STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = blockIdx.x >> 1;
+    const int tm = pair / ntn, tn = pair % ntn;
+    const int m0 = tm * 2 * TM + (int)rank * TM;  // this CTA's rows (relative to the a-split buffer)
+    const int nb = tn * TN + (int)rank * P_BN;     // this CTA's half of the B columns
+    const int n0 = tn * TN;                         // output columns of the pair tile
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer (both CTAs): this CTA's halves, completing on the leader's full barrier
+        for (int kb = 0; kb < kslabs; kb++) {
+            const int s = kb % P_STAGES;
+            mbar_wait(&empty[s], ((kb / P_STAGES) & 1) ^ 1);
+            unsigned char *st = smem + s * P_STAGE_BYTES;
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+            const int kc = kb * TK;
+            tma_load_2d_2sm(st, &map_ahi, &full[s], kc, m0);
+            tma_load_2d_2sm(st + A_BYTES, &map_alo, &full[s], kc, m0);
+            tma_load_2d_2sm(st + 2 * A_BYTES, &map_bhi, &full[s], kc, nb);
+            tma_load_2d_2sm(st + 2 * A_BYTES + P_B_BYTES, &map_blo, &full[s], kc, nb);
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+        // ---- MMA issuer (leader only): M = 256 across the pair, N = 256
+        constexpr uint32_t idesc = idesc_tf32(2 * TM, TN);
+        for (int kb = 0; kb < kslabs; kb++) {
+            const int s = kb % P_STAGES;
+            mbar_wait(&full[s], (kb / P_STAGES) & 1);
+            tc_fence_after();
+            unsigned char *st = smem + s * P_STAGE_BYTES;
+            const uint64_t ahi = smem_desc_sw128(st), alo = smem_desc_sw128(st + A_BYTES);
+            const uint64_t bhi = smem_desc_sw128(st + 2 * A_BYTES), blo = smem_desc_sw128(st + 2 * A_BYTES + P_B_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < TK / 8; kk++) {
+                const uint64_t adv = (uint64_t)(kk * 32) >> 4;
+                mma_tf32_2sm(tmem, alo + adv, bhi + adv, idesc, (kb | kk) != 0);
+                mma_tf32_2sm(tmem, ahi + adv, blo + adv, idesc, 1);
+                mma_tf32_2sm(tmem, ahi + adv, bhi + adv, idesc, 1);
+            }
+            mma_commit_pair(&empty[s]);  // slab s free in both CTAs once these MMAs retire
+        }
+        mma_commit_pair(done);  // both accumulators complete
+    }
+    __syncwarp();
+
+    // ---- epilogue: each CTA's 4 warps, TMEM lanes = this CTA's 128 rows
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int64_t row = m0 + warp * 32 + lane;
+    float *crow = c + row * ldc + n0;
+#pragma unroll 1
+    for (int cc = 0; cc < TN; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)cc, r);
+        float4 *dst = reinterpret_cast<float4 *>(crow + cc);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            float4 v = dst[q];
+            v.x += __uint_as_float(r[4 * q + 0]);
+            v.y += __uint_as_float(r[4 * q + 1]);
+            v.z += __uint_as_float(r[4 * q + 2]);
+            v.w += __uint_as_float(r[4 * q + 3]);
+            dst[q] = v;
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's barriers
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
 // ---- host side -------------------------------------------------------------------
 
 typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -299,15 +452,26 @@ int launch_matmul_tf32x3(const float *a, const float *b, float *c, int64_t n, in
         if ((rc = make_map(&mahi, ahi, M, K, TM)) || (rc = make_map(&malo, alo, M, K, TM)) ||
             (rc = make_map(&mbhi, bhi, Nc, K, TN)) || (rc = make_map(&mblo, blo, Nc, K, TN)))
             goto out;
-        rc = allow_smem((const void *)k_tf32x3, SMEM_BYTES);
-        if (rc) goto out;
         const int ntn = (int)(Nc / TN);
-        const int64_t tiles = (M / TM) * ntn;
-        // the kernel's TMA row coordinate is relative to the a-split buffer (rows 0..M);
+        // the kernels' TMA row coordinate is relative to the a-split buffer (rows 0..M);
         // c rows are offset by rlo
-        k_tf32x3<<<(unsigned)tiles, 128, SMEM_BYTES, st>>>(mahi, malo, mbhi, mblo, c + rlo * n, n, 0, ntn,
-                                                           (int)(K / TK));
-        rc = after_launch("matmul_tf32x3");
+        if (M % (2 * TM) == 0 && getenv("PK_TF32_1SM") == nullptr) {  // CTA pairs: 256 x 256 tiles
+            CUtensorMap mbhi2, mblo2;
+            if ((rc = make_map(&mbhi2, bhi, Nc, K, P_BN)) || (rc = make_map(&mblo2, blo, Nc, K, P_BN))) goto out;
+            rc = allow_smem((const void *)k_tf32x3_pair, P_SMEM_BYTES);
+            if (rc) goto out;
+            const int64_t pairs = (M / (2 * TM)) * ntn;
+            k_tf32x3_pair<<<(unsigned)(2 * pairs), 128, P_SMEM_BYTES, st>>>(mahi, malo, mbhi2, mblo2, c + rlo * n, n,
+                                                                          ntn, (int)(K / TK));
+            rc = after_launch("matmul_tf32x3_pair");
+        } else {
+            rc = allow_smem((const void *)k_tf32x3, SMEM_BYTES);
+            if (rc) goto out;
+            const int64_t tiles = (M / TM) * ntn;
+            k_tf32x3<<<(unsigned)tiles, 128, SMEM_BYTES, st>>>(mahi, malo, mbhi, mblo, c + rlo * n, n, 0, ntn,
+                                                               (int)(K / TK));
+            rc = after_launch("matmul_tf32x3");
+        }
     }
 out:
     cudaFreeAsync(ws, st);
