@@ -291,7 +291,13 @@ int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void 
 
 namespace {
 
-constexpr int kMaxChunks = 8;                  // pipeline depth limit of pk_run_host
+#ifndef PK_RH_CHUNKS
+#define PK_RH_CHUNKS 8
+#endif
+#ifndef PK_RH_SLICES
+#define PK_RH_SLICES 4
+#endif
+constexpr int kMaxChunks = PK_RH_CHUNKS;                  // pipeline depth limit of pk_run_host
 constexpr int kMaxDevices = 64;                // pk_launch_multi
 constexpr int64_t kChunkBytes = 48ll << 20;    // PCIe bytes per chunk (~1 ms of transfer)
 
@@ -309,7 +315,7 @@ bool chunkable(const pk_launch_t &L) {
     }
 }
 
-constexpr int kSlices = 4;  // reduction slices of matmul's first row chunk
+constexpr int kSlices = PK_RH_SLICES;  // reduction slices of matmul's first row chunk
 
 struct HostRun {
     cudaStream_t h2d = nullptr, d2h = nullptr, cs[kMaxChunks] = {};
