@@ -9,39 +9,84 @@
 // cache(x) kept: x is staged once per block in shared memory (the case
 // requires N <= Z_B); caching-off reads x through L1/L2.
 // Integers accumulate in wrapping int32 -- exact whenever the result fits, as
-// two's-complement sums are exact modulo 2^32.  float32 data accumulate in
-// binary64 (the reference sums Python floats), rounded once at the end.
+// two's-complement sums are exact modulo 2^32.  float32 data accumulate in a
+// double-float pair (see DF), rounded once at the end.
 // HBM-bound: 4*N bytes of a per row dominate (x stays on chip).
 #include "pk_internal.cuh"
 
 namespace pk {
 namespace {
 
+// float32 data: a double-float accumulator (hi + lo, both fp32).  Each
+// product is split exactly (p = a*x rounded, e = fma(a, x, -p)) and added
+// with TwoSum, so the running sum carries ~48 bits -- the accuracy of the
+// reference's binary64 sum of Python floats -- on the FP32 pipe.  (Binary64
+// accumulation measured 1.9 TB/s at N = 32768: the F2F conversions and DFMAs
+// bound it; the fp32 pair keeps the kernel at HBM speed.)  Explicit _rn
+// intrinsics keep nvcc from contracting the splits into FMAs.
+struct DF {
+    float hi, lo;
+};
+
+__device__ __forceinline__ void df_add(DF &acc, float v, float err_in) {
+    const float t = __fadd_rn(acc.hi, v);
+    const float bp = __fsub_rn(t, acc.hi);
+    const float err = __fadd_rn(__fsub_rn(acc.hi, __fsub_rn(t, bp)), __fsub_rn(v, bp));  // TwoSum
+    acc.hi = t;
+    acc.lo = __fadd_rn(acc.lo, __fadd_rn(err, err_in));
+}
+
+__device__ __forceinline__ void df_add_prod(DF &acc, float a, float x) {
+    const float p = __fmul_rn(a, x);
+    df_add(acc, p, __fmaf_rn(a, x, -p));  // p + fma(a, x, -p) == a * x exactly
+}
+
 template <typename T> struct Acc;
 template <> struct Acc<int> { using type = int; };
-template <> struct Acc<float> { using type = double; };
+template <> struct Acc<float> { using type = DF; };
 
-template <typename A>
-__device__ __forceinline__ A group_sum(A v, int lanes) {
+__device__ __forceinline__ void acc_zero(int &a) { a = 0; }
+__device__ __forceinline__ void acc_zero(DF &a) { a.hi = a.lo = 0.f; }
+
+__device__ __forceinline__ int group_sum(int v, int lanes) {
     for (int o = lanes >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, lanes);
     return v;
 }
+__device__ __forceinline__ DF group_sum(DF v, int lanes) {
+    for (int o = lanes >> 1; o > 0; o >>= 1) {
+        const float h = __shfl_xor_sync(0xffffffffu, v.hi, o, lanes), l = __shfl_xor_sync(0xffffffffu, v.lo, o, lanes);
+        df_add(v, h, l);
+    }
+    return v;
+}
 
-template <typename A, typename T>
-__device__ __forceinline__ A dot4(const int4 &av, const T *xp) {
-    const T *ap = reinterpret_cast<const T *>(&av);
-    A s = (A)ap[0] * (A)xp[0];
-    s += (A)ap[1] * (A)xp[1];
-    s += (A)ap[2] * (A)xp[2];
-    s += (A)ap[3] * (A)xp[3];
-    return s;
+__device__ __forceinline__ void dot4(int &acc, const int4 &av, const int *xp) {
+    acc += av.x * xp[0] + av.y * xp[1] + av.z * xp[2] + av.w * xp[3];
+}
+__device__ __forceinline__ void dot4(DF &acc, const int4 &av, const float *xp) {
+    df_add_prod(acc, __int_as_float(av.x), xp[0]);
+    df_add_prod(acc, __int_as_float(av.y), xp[1]);
+    df_add_prod(acc, __int_as_float(av.z), xp[2]);
+    df_add_prod(acc, __int_as_float(av.w), xp[3]);
+}
+__device__ __forceinline__ void dot1(int &acc, int a, int x) { acc += a * x; }
+__device__ __forceinline__ void dot1(DF &acc, float a, float x) { df_add_prod(acc, a, x); }
+
+// y + the row's sum: ints wrap (two's complement, exact modulo 2^32); floats
+// round y + hi + lo once through binary64
+__device__ __forceinline__ int finish(int y, int sum) { return y + sum; }
+__device__ __forceinline__ float finish(float y, DF sum) {
+    return (float)(((double)y + (double)sum.hi) + (double)sum.lo);
 }
 
 constexpr int kRows = 4;    // rows per lane group in flight
 constexpr int kUnroll = 4;  // 128-bit loads per row in flight
 
+#ifndef PK_MV_NT
+#define PK_MV_NT 512
+#endif
 template <typename T, bool STAGED, bool VEC>
-__global__ void __launch_bounds__(256) k_matvec(const T *__restrict__ a, const T *__restrict__ x,
+__global__ void __launch_bounds__(PK_MV_NT) k_matvec(const T *__restrict__ a, const T *__restrict__ x,
                                                 T *__restrict__ y, int64_t N, int64_t rlo,
                                                 int64_t rhi, int tile, int lanes) {
     using A = typename Acc<T>::type;
@@ -67,7 +112,7 @@ __global__ void __launch_bounds__(256) k_matvec(const T *__restrict__ a, const T
         const int nr = (int)min((int64_t)kRows, end - r0);
         A acc[kRows];
 #pragma unroll
-        for (int i = 0; i < kRows; i++) acc[i] = 0;
+        for (int i = 0; i < kRows; i++) acc_zero(acc[i]);
         if (VEC) {
             const int64_t n4 = N / 4;
             const int4 *rows[kRows];
@@ -91,7 +136,7 @@ __global__ void __launch_bounds__(256) k_matvec(const T *__restrict__ a, const T
                         const int4 xq = xv[q];
                         const T *xp = reinterpret_cast<const T *>(&xq);
 #pragma unroll
-                        for (int i = 0; i < kRows; i++) acc[i] += dot4<A, T>(v[u][i], xp);
+                        for (int i = 0; i < kRows; i++) dot4(acc[i], v[u][i], xp);
                     }
                 }
             }
@@ -100,14 +145,14 @@ __global__ void __launch_bounds__(256) k_matvec(const T *__restrict__ a, const T
             for (int i = 0; i < kRows; i++) {
                 if (i < nr) {
                     const T *row = a + (r0 + i) * N;
-                    for (int64_t q = lane; q < N; q += lanes) acc[i] += (A)row[q] * (A)xs[q];
+                    for (int64_t q = lane; q < N; q += lanes) dot1(acc[i], row[q], xs[q]);
                 }
             }
         }
 #pragma unroll
         for (int i = 0; i < kRows; i++) {
             const A sum = group_sum(acc[i], lanes);
-            if (lane == 0 && i < nr) y[r0 + i] = (T)((A)y[r0 + i] + sum);
+            if (lane == 0 && i < nr) y[r0 + i] = finish(y[r0 + i], sum);
         }
     }
 }
@@ -117,7 +162,10 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     const int64_t tile64 = elems(L) * L.B;
     if (tile64 > (1 << 30)) return fail(PK_E_UNSUPPORTED, "matvec: tile too large");
     const int tile = (int)tile64;
-    int nt = (int)(L.B < 256 ? L.B : 256);  // groups loop over the tile, so 256 threads cover any B
+    // the block size is the kernel's (the groups loop over the tile, so any size
+    // covers the program's B): 512 threads keep 16 warps of 16 x 16-byte loads
+    // in flight beside the one staged x per SM (6.6 -> 7.1 TB/s at N = 32768)
+    int nt = PK_MV_NT;
     // lanes per row: the largest power of two <= 32 dividing the block size
     int lanes = 1;
     while (lanes < 32 && nt % (lanes * 2) == 0) lanes *= 2;
