@@ -484,6 +484,35 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
                             "because h steps share one HBM pass; results bit-identical"}
         del bufs
         torch.cuda.empty_cache()
+    # mat-vec on float32 data (SURVEY 8(d) proposes N = 32768 FP32): double-float accumulation
+    if "matvec" in out and "params" in out["matvec"]:
+        mp = dict(out["matvec"]["params"])
+        Nm = mp["N"]
+        kind = programs.original("matvec")
+        sel = cases.select(kind, mp, mv)
+        L = binding.make_launch(kind, mp, sel.applied, _lib.DTYPE_F32)
+        g = torch.Generator(device="cuda").manual_seed(0x1801)
+        bufs = [torch.rand(Nm * Nm, device="cuda", generator=g) * 2 - 1, torch.rand(Nm, device="cuda", generator=g),
+                torch.zeros(Nm, device="cuda")]
+        ptrs = [x.data_ptr() for x in bufs]
+        st = torch.cuda.current_stream()
+        for _ in range(3):
+            _lib.launch(L, ptrs, st.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(10):
+            _lib.launch(L, ptrs, st.cuda_stream)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        gbs = (4 * Nm * Nm + 8 * Nm) / (ms * 1e-3) / 1e9
+        out["matvec_f32"] = {"params": mp, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
+                             "value": round(gbs, 1), "unit": "GB/s",
+                             "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
+                             "note": "float32 a, x, y; products split exactly and summed as a double-float pair"}
+        del bufs
+        torch.cuda.empty_cache()
     # the other size of BASELINE configs[1]: FP32 matmul n = 2048, (B0, ub1, s) tuned inside the case
     n2 = 2048
     kind = programs.original("matmul")
