@@ -233,9 +233,17 @@ def main() -> int:
     rank, world, local = dist_info()
     if world != args.gpus and world > 1:
         print("warning: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus), file=sys.stderr)
+    # test hook: PK_BENCH_ONE_GPU=1 maps every rank onto device 0 over gloo (the N > 1 code
+    # path on a one-GPU box; NCCL refuses two ranks on one device)
+    one_gpu = os.environ.get("PK_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     peaks = load_peaks()
     mv = machine_mod.live(local)

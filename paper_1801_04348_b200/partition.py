@@ -105,13 +105,22 @@ class TorchExchanger(Exchanger):
 
     def exchange(self, ops):
         d = self.dist
-        p2p = []
+        # gloo moves host memory only: CUDA slices are staged through host copies
+        staged = d.get_backend(self.group) == "gloo"
+        p2p, back = [], []
         for kind, t, peer in ops:
+            buf = t
+            if staged and t.is_cuda:
+                buf = t.cpu() if kind == "send" else t.new_empty(t.shape, device="cpu")
+                if kind == "recv":
+                    back.append((t, buf))
             fn = d.isend if kind == "send" else d.irecv
-            p2p.append(d.P2POp(fn, t, peer, group=self.group))
+            p2p.append(d.P2POp(fn, buf, peer, group=self.group))
         if p2p:
             for req in d.batch_isend_irecv(p2p):
                 req.wait()
+        for t, buf in back:
+            t.copy_(buf)
 
 
 class LocalExchanger(Exchanger):
