@@ -149,10 +149,13 @@ int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo
  * global indexing -- dev_ptrs[k * nptrs + i] is array i on device k -- with
  * the inputs present on every device, and computes its aligned share of the
  * units (rows; elements for reversal; interior positions / rows for the
- * stencils).  The row families need no exchange.  The stencils refresh
- * ghost zones of width `halo` (<= 0: 16; capped by the smallest slab and T)
- * every `halo` steps with peer copies (cudaMemcpyPeerAsync: NVLink between
- * B200s), recomputing the overlap in between.  With gather != 0 every
+ * stencils).  The row families need no exchange.  The stencils (halo <= 0)
+ * run the sweep with the halo exchange fused in (pk_jacobi_sweep_peer with
+ * direct peer pointers: edge blocks store into the neighbours' buffers over
+ * NVLink, device counters order the devices); with halo > 0 -- or layouts /
+ * devices the fused sweep does not take -- they refresh ghost zones of width
+ * `halo` (capped by the smallest slab and T) every `halo` steps with peer
+ * copies (cudaMemcpyPeerAsync), recomputing the overlap in between.  With gather != 0 every
  * device's written share (both Jacobi halves) is copied into devices[0]'s
  * arrays, which then hold the whole result, bit-identical to pk_launch.
  * L->lo / L->hi must be 0.  Synchronises every device. */

@@ -742,6 +742,68 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         share(u0, u1, align, k, ndev, &lo[k], &hi[k]);
         if (hi[k] - lo[k] < min_slab) min_slab = hi[k] - lo[k];
     }
+    // Default (halo <= 0): the halo exchange fused into the sweep -- every
+    // device's edge blocks store their rows straight into the neighbours'
+    // buffers (peer pointers, NVLink) and order themselves with device
+    // counters (pk_jacobi_sweep_peer), ghost width 1, no copies or events per
+    // step.  An explicit halo width keeps the ghost zones refreshed by peer
+    // copies every h steps (below); so do layouts the register sweeps do not
+    // take and devices without peer access.
+    bool fused = halo <= 0 && min_slab > 0 && getenv("PK_MULTI_COPY") == nullptr;
+    for (int k = 0; k < ndev && fused; k++) {
+        const uintptr_t base = reinterpret_cast<uintptr_t>(ptrs(k)[0]);
+        fused = one ? (base & 3u) == 0 : ((N & 1) == 0 && (base & 15u) == 0);
+        for (int j = k - 1; j <= k + 1 && fused; j += 2) {
+            if (j < 0 || j >= ndev || devices[j] == devices[k]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, devices[k], devices[j]);
+            fused = can != 0;
+        }
+    }
+    if (fused) {
+        unsigned *ctr[kMaxDevices] = {};
+        for (int k = 0; k < ndev && rc == PK_OK; k++) {  // [from_left, from_right, error] per device
+            cudaSetDevice(devices[k]);
+            cudaError_t e = cudaMallocAsync((void **)&ctr[k], 4 * sizeof(unsigned), M.st[k]);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ctr[k], 0, 4 * sizeof(unsigned), M.st[k]);
+            if (e == cudaSuccess) e = cudaEventRecord(M.done[k], M.st[k]);
+            if (e != cudaSuccess) rc = fail(PK_E_CUDA, "peer counters on device %d: %s", devices[k], cudaGetErrorString(e));
+        }
+        for (int k = 0; k < ndev && rc == PK_OK; k++) {  // no signal before a neighbour's counters are zero
+            cudaSetDevice(devices[k]);
+            if (k > 0) cudaStreamWaitEvent(M.st[k], M.done[k - 1], 0);
+            if (k + 1 < ndev) cudaStreamWaitEvent(M.st[k], M.done[k + 1], 0);
+        }
+        for (int64_t t = 0; t < L->T && rc == PK_OK; t++) {
+            for (int k = 0; k < ndev && rc == PK_OK; k++) {
+                cudaSetDevice(devices[k]);
+                pk_peer_t P = {};
+                P.left_base = k > 0 ? ptrs(k - 1)[0] : nullptr;
+                P.right_base = k + 1 < ndev ? ptrs(k + 1)[0] : nullptr;
+                P.wait_left = ctr[k];
+                P.wait_right = ctr[k] + 1;
+                P.signal_left = k > 0 ? ctr[k - 1] + 1 : nullptr;   // the left neighbour's from_right
+                P.signal_right = k + 1 < ndev ? ctr[k + 1] : nullptr;  // the right neighbour's from_left
+                P.error = ctr[k] + 2;
+                rc = jacobi_sweep_peer(Ln, static_cast<int *>(ptrs(k)[0]), t, lo[k], hi[k], P, M.st[k]);
+            }
+        }
+        unsigned err = 0;
+        for (int k = 0; k < ndev; k++) {
+            if (!ctr[k]) continue;
+            cudaSetDevice(devices[k]);
+            unsigned v = 0;
+            if (cudaMemcpyAsync(&v, ctr[k] + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, M.st[k]) == cudaSuccess &&
+                cudaStreamSynchronize(M.st[k]) == cudaSuccess)
+                err |= v;
+        }
+        for (int k = 0; k < ndev; k++) {  // every device done before any counter goes away
+            if (!ctr[k]) continue;
+            cudaSetDevice(devices[k]);
+            cudaFreeAsync(ctr[k], M.st[k]);
+        }
+        if (rc == PK_OK && err) rc = fail(PK_E_CUDA, "pk_launch_multi: a peer wait timed out");
+    }
     int64_t h = halo > 0 ? halo : 16;
     if (h > min_slab) h = min_slab;
     if (h > L->T) h = L->T;
@@ -752,7 +814,7 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         const bool upper = one ? (t % 2 == 0) : (t % 2 == 1);
         return upper ? a + half : a;
     };
-    for (int64_t t = 0; t < L->T && rc == PK_OK;) {
+    for (int64_t t = fused ? L->T : 0; t < L->T && rc == PK_OK;) {
         const int64_t hb = (L->T - t) < h ? (L->T - t) : h;
         // exchange: the ghost rows of s(t) on both sides of every boundary; the
         // source device waits before overwriting them (step t+1 writes s(t))

@@ -224,11 +224,14 @@ def test_run_rows_with_pk_launcher(cuda, oracle_mod, family, params):
     ("jacobi2d", {"T": 21, "N": 130, "s": 2, "B0": 4, "B1": 8}),
     ("jacobi2d", {"T": 6, "N": 67, "s": 1, "B0": 2, "B1": 16}),
 ])
-@pytest.mark.parametrize("ndev,halo", [(2, 0), (3, 4), (4, 1)])
+@pytest.mark.parametrize("ndev,halo", [(2, 0), (3, 0), (4, 0), (3, 4), (4, 1)])
 def test_launch_multi_matches_oracle(cuda, oracle_mod, family, params, ndev, halo):
     """pk_launch_multi over 'devices' that all map to GPU 0 (separate buffers,
     peer copies become device copies): shares, ghost-zone exchanges and the
-    gather give the oracle's result on devices[0]."""
+    gather give the oracle's result on devices[0].  halo = 0: the stencils'
+    exchange fused into the sweep (edge blocks store into the neighbours'
+    buffers, device counters order the devices); halo > 0: ghost zones of
+    that width refreshed by peer copies."""
     from paper_1801_04348_b200 import programs, run_program
 
     kind = programs.original(family)
@@ -237,7 +240,7 @@ def test_launch_multi_matches_oracle(cuda, oracle_mod, family, params, ndev, hal
     init = {}
     for k, s in shapes.items():
         if family == "jacobi" or family == "jacobi2d":
-            init[k] = rng.integers(-(2**31), 2**31 - 1, size=s).astype(np.int32) if halo == 1 else \
+            init[k] = rng.integers(-(2**31), 2**31 - 1, size=s).astype(np.int32) if halo == 1 or ndev == 4 else \
                 rng.integers(-1000, 1000, size=s).astype(np.int32)
         else:
             init[k] = rng.integers(-40, 40, size=s).astype(np.int32)
