@@ -22,6 +22,7 @@ cap jacobi2d_tma k_jacobi2d_tma 3 jacobi2d '{"T": 4, "N": 16386, "s": 32, "B0": 
 cap jacobi2d_temporal k_jacobi2d_wavefront 0 jacobi2d '{"T": 8, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1 --temporal=7
 cap reverse k_reverse 1 reverse '{"N": 1073741824, "s": 16, "B": 256}' 3
 cap transpose k_transpose 1 transpose '{"N": 32768, "s": 8, "B0": 64, "B1": 8}' 3
-cap matvec k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 256}' 3
+cap matvec k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 512}' 3
+cap matvec_f32 k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 512}' 3 --f32
 cap temporal k_jacobi1d_rtemporal 0 jacobi '{"T": 16, "N": 268435458, "s": 16, "B": 256}' 1 --temporal=15
 ls -la $D
