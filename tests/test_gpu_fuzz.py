@@ -54,3 +54,32 @@ def test_random_parameters_match_oracle(cuda, oracle_mod, family):
             assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), \
                 (family, P, case, generic, name)
         done += 1
+
+
+EMPTY = {
+    "reverse": [{"N": 0, "s": 2, "B": 32}, {"N": 5, "s": 2, "B": 32}],
+    "transpose": [{"N": 0, "s": 1, "B0": 4, "B1": 4}, {"N": 3, "s": 2, "B0": 4, "B1": 4}],
+    "jacobi": [{"T": 3, "N": 2, "s": 1, "B": 4}, {"T": 0, "N": 50, "s": 1, "B": 4}, {"T": 2, "N": 5, "s": 2, "B": 4}],
+    "jacobi2d": [{"T": 2, "N": 2, "s": 1, "B0": 2, "B1": 2}, {"T": 0, "N": 9, "s": 1, "B0": 2, "B1": 2}],
+    "matvec": [{"N": 0, "s": 1, "B": 32}, {"N": 7, "s": 1, "B": 32}],
+    "matmul": [{"n": 0, "B0": 4, "ub1": 2, "s": 2}, {"n": 3, "B0": 4, "ub1": 2, "s": 2}],
+    "addition": [{"N": 0, "B0": 2, "B1": 2}, {"N": 3, "B0": 4, "B1": 4}],
+}
+
+
+@pytest.mark.parametrize("family", sorted(EMPTY))
+def test_empty_arrays_and_no_covered_block(cuda, oracle_mod, family):
+    """Zero-sized arrays, extents below one block (the grid covers nothing),
+    T = 0 and stencils without interior: nothing is launched that could fail,
+    and every array comes back as the reference leaves it."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    kind = programs.original(family)
+    rng = np.random.default_rng(5)
+    for P in EMPTY[family]:
+        shapes = programs.array_shapes(kind, P)
+        arrays = {k: rng.integers(-100, 100, size=s).astype(np.int32) for k, s in shapes.items()}
+        want = oracle_mod.run(family, P, arrays)
+        got = run_program(kind.text, P, arrays)
+        for name in shapes:
+            assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), (P, name)
