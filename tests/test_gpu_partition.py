@@ -248,3 +248,31 @@ def test_launch_multi_matches_oracle(cuda, oracle_mod, family, params, ndev, hal
     got = run_program(programs.source(family), params, init, devices=[0] * ndev, halo=halo)
     for name in programs.FAMILIES[family].written:
         assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), name
+
+
+@pytest.mark.parametrize("family,params", [
+    ("reverse", {"N": 0, "s": 2, "B": 32}), ("reverse", {"N": 5, "s": 2, "B": 32}),
+    ("matmul", {"n": 0, "B0": 4, "ub1": 2, "s": 2}), ("matmul", {"n": 3, "B0": 4, "ub1": 2, "s": 2}),
+    ("matvec", {"N": 0, "s": 1, "B": 32}), ("transpose", {"N": 3, "s": 2, "B0": 4, "B1": 4}),
+    ("addition", {"N": 0, "B0": 2, "B1": 2}),
+    ("jacobi", {"T": 3, "N": 2, "s": 1, "B": 4}), ("jacobi", {"T": 0, "N": 50, "s": 1, "B": 4}),
+    ("jacobi", {"T": 5, "N": 1001, "s": 2, "B": 32}),
+    ("jacobi2d", {"T": 2, "N": 2, "s": 1, "B0": 2, "B1": 2}), ("jacobi2d", {"T": 3, "N": 67, "s": 2, "B0": 4, "B1": 8}),
+])
+def test_run_host_edge_sizes_match_oracle(cuda, oracle_mod, family, params):
+    """The host-buffer entry point on empty arrays, extents below one block,
+    T = 0, stencils without interior and odd stencil sizes: the host
+    buffers end as the oracle leaves them."""
+    from paper_1801_04348_b200 import _lib, binding, cases, programs
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    rng = np.random.default_rng(21)
+    init = {k: rng.integers(-1000, 1000, size=s).astype(np.int32) for k, s in shapes.items()}
+    want = oracle_mod.run(family, params, init)
+    host = {k: np.ascontiguousarray(v.copy()) for k, v in init.items()}
+    sel = cases.select(kind, params, "nominal")
+    L = binding.make_launch(kind, params, sel.applied)
+    _lib.run_host(L, [host[a.name].ctypes.data for a in programs.FAMILIES[family].arrays], 0)
+    for name in shapes:
+        assert np.array_equal(host[name].reshape(-1), np.asarray(want[name]).reshape(-1)), name
