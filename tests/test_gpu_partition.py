@@ -276,3 +276,27 @@ def test_run_host_edge_sizes_match_oracle(cuda, oracle_mod, family, params):
     _lib.run_host(L, [host[a.name].ctypes.data for a in programs.FAMILIES[family].arrays], 0)
     for name in shapes:
         assert np.array_equal(host[name].reshape(-1), np.asarray(want[name]).reshape(-1)), name
+
+
+@pytest.mark.parametrize("family,params", [
+    ("reverse", {"N": 0, "s": 2, "B": 32}), ("reverse", {"N": 200, "s": 2, "B": 32}),
+    ("matmul", {"n": 0, "B0": 4, "ub1": 2, "s": 2}), ("matmul", {"n": 9, "B0": 4, "ub1": 2, "s": 2}),
+    ("matvec", {"N": 5, "s": 1, "B": 2}), ("transpose", {"N": 6, "s": 1, "B0": 2, "B1": 2}),
+    ("jacobi", {"T": 3, "N": 2, "s": 1, "B": 4}), ("jacobi", {"T": 4, "N": 14, "s": 1, "B": 4}),
+    ("jacobi", {"T": 0, "N": 50, "s": 1, "B": 4}),
+    ("jacobi2d", {"T": 2, "N": 2, "s": 1, "B0": 2, "B1": 2}), ("jacobi2d", {"T": 3, "N": 8, "s": 1, "B0": 2, "B1": 2}),
+])
+@pytest.mark.parametrize("ndev", [3, 4])
+def test_launch_multi_fewer_units_than_devices(cuda, oracle_mod, family, params, ndev):
+    """More devices than units (some devices get empty shares), empty arrays,
+    T = 0, stencils without interior: the oracle's result on devices[0]."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    kind = programs.original(family)
+    shapes = programs.array_shapes(kind, params)
+    rng = np.random.default_rng(ndev)
+    init = {k: rng.integers(-1000, 1000, size=s).astype(np.int32) for k, s in shapes.items()}
+    want = oracle_mod.run(family, params, init)
+    got = run_program(programs.source(family), params, init, devices=[0] * ndev)
+    for name in shapes:
+        assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), name
