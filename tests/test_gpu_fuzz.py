@@ -1,6 +1,9 @@
 """Randomised parity: many small parameter draws per family (tails, odd
 extents, block sizes that are not warp multiples, every leaf), CUDA vs the
-CPU oracle, bit-exact.  Seeds are fixed so failures reproduce."""
+CPU oracle, bit-exact.  Seeds are fixed so failures reproduce; PK_FUZZ_DRAWS
+and PK_FUZZ_SEED widen a run (long soak runs on the GPU box)."""
+
+import os
 
 import numpy as np
 import pytest
@@ -35,11 +38,11 @@ def _threads_ok(family, P):
 def test_random_parameters_match_oracle(cuda, oracle_mod, family):
     from paper_1801_04348_b200 import case_table, programs, run_program
 
-    rng = np.random.default_rng(0xF022 + hash(family) % 1000)
+    rng = np.random.default_rng(0xF022 + sum(map(ord, family)) + 7919 * int(os.environ.get("PK_FUZZ_SEED", 0)))
     kind = programs.original(family)
     ncases = len(case_table(family, "b200").cases)
     done = 0
-    while done < 25:
+    while done < int(os.environ.get("PK_FUZZ_DRAWS", 25)):
         P = _draw(family, rng)
         if not _threads_ok(family, P):
             continue
