@@ -86,3 +86,38 @@ def test_empty_arrays_and_no_covered_block(cuda, oracle_mod, family):
         got = run_program(kind.text, P, arrays)
         for name in shapes:
             assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), (P, name)
+
+
+@pytest.mark.parametrize("family", ["matvec", "matmul"])
+def test_random_float32_within_tolerance(cuda, oracle_mod, family):
+    """float32 draws for the accumulating families against the binary64
+    oracle: matmul within max(1e-5*K/1024, 2*K*2^-24) of max sum|a||b|,
+    mat-vec within 2 ulps (+2^-40 sum|a x| for cancelling rows)."""
+    from paper_1801_04348_b200 import case_table, programs, run_program
+
+    rng = np.random.default_rng(0xF1 + sum(map(ord, family)) + 7919 * int(os.environ.get("PK_FUZZ_SEED", 0)))
+    kind = programs.original(family)
+    ncases = len(case_table(family, "b200").cases)
+    done = 0
+    while done < int(os.environ.get("PK_FUZZ_DRAWS", 25)):
+        P = _draw(family, rng)
+        if not _threads_ok(family, P):
+            continue
+        shapes = programs.array_shapes(kind, P)
+        arrays = {k: rng.uniform(-1, 1, size=s).astype(np.float32) for k, s in shapes.items()}
+        want = np.asarray(oracle_mod.run(family, P, arrays)["y" if family == "matvec" else "c"], dtype=np.float64)
+        case = int(rng.integers(1, ncases + 1))
+        generic = bool(rng.integers(0, 2))
+        got = run_program(kind.text, P, arrays, case=case, generic=generic)
+        g = np.asarray(got["y" if family == "matvec" else "c"], dtype=np.float64).reshape(want.shape)
+        if family == "matmul":
+            a, b = arrays["a"].astype(np.float64), arrays["b"].astype(np.float64)
+            scale = max((np.abs(a) @ np.abs(b)).max() if P["n"] else 0.0, 1e-30)
+            K = max(1, P["n"])
+            assert np.abs(g - want).max(initial=0.0) / scale <= max(1e-5 * K / 1024.0, 2.0 * K * 2.0**-24), \
+                (P, case, generic)
+        else:
+            a, x = arrays["a"].astype(np.float64), arrays["x"].astype(np.float64)
+            mag = np.abs(arrays["y"].astype(np.float64)) + np.abs(a) @ np.abs(x)
+            assert np.all(np.abs(g - want) <= 2.0 * 2.0**-24 * np.abs(want) + 2.0**-40 * mag), (P, case, generic)
+        done += 1
