@@ -121,3 +121,32 @@ def test_random_float32_within_tolerance(cuda, oracle_mod, family):
             mag = np.abs(arrays["y"].astype(np.float64)) + np.abs(a) @ np.abs(x)
             assert np.all(np.abs(g - want) <= 2.0 * 2.0**-24 * np.abs(want) + 2.0**-40 * mag), (P, case, generic)
         done += 1
+
+
+@pytest.mark.parametrize("family", ["jacobi", "jacobi2d"])
+def test_random_temporal_blocking_matches_oracle(cuda, oracle_mod, family):
+    """Temporally blocked stencils (register-resident 1-D, register wavefront
+    2-D, and their shared-memory fallbacks for odd N) over random extents,
+    step counts and block depths h, narrow and full-range values: bit-exact."""
+    from paper_1801_04348_b200 import programs, run_program
+
+    rng = np.random.default_rng(0x7E + sum(map(ord, family)) + 7919 * int(os.environ.get("PK_FUZZ_SEED", 0)))
+    kind = programs.original(family)
+    done = 0
+    while done < int(os.environ.get("PK_FUZZ_DRAWS", 25)):
+        P = _draw(family, rng)
+        if family == "jacobi":
+            P["N"] = int(rng.integers(2, 40000))
+        else:
+            P["N"] = int(rng.integers(3, 400))
+        P["T"] = int(rng.integers(0, 40))
+        if not _threads_ok(family, P):
+            continue
+        h = int(rng.integers(1, 17 if family == "jacobi" else 9))
+        lim = 1 << 20 if rng.integers(0, 2) else 2**31 - 1
+        shapes = programs.array_shapes(kind, P)
+        arrays = {k: rng.integers(-lim, lim, size=s, dtype=np.int64).astype(np.int32) for k, s in shapes.items()}
+        want = oracle_mod.run(family, P, arrays)["a"]
+        got = run_program(kind.text, P, arrays, temporal=h)["a"]
+        assert np.array_equal(np.asarray(got).reshape(-1), np.asarray(want).reshape(-1)), (P, h, lim)
+        done += 1
