@@ -59,8 +59,17 @@ extern "C" {
                                    on the device and pk_jacobi_sweep forms 64-bit sums     */
 
 /* ---- element types ------------------------------------------------------- */
-#define PK_DTYPE_I32 0 /* the DSL's int: C int32 arithmetic, truncating / and % */
-#define PK_DTYPE_F32 1 /* float32 storage (matmul/matvec: Python floats in the reference) */
+#define PK_DTYPE_I32 0 /* the DSL's int: C int32 arithmetic, truncating / and %; 4-byte words     */
+#define PK_DTYPE_F32 1 /* float32 storage: FFMA matmul, double-float mat-vec, IEEE add; 4-byte words */
+#define PK_DTYPE_I64 2 /* int64: reverse/transpose move 8-byte words; addition/matvec/matmul compute
+                          in wrapping int64 (exact whenever the result fits, like the reference's
+                          unbounded ints)                                                          */
+#define PK_DTYPE_F64 3 /* binary64, the reference's Python float: reverse/transpose move 8-byte
+                          words; addition/matvec/matmul evaluate c + a*b with one rounding per
+                          operation in the interpreter's order (no contraction): bit-identical
+                          to interp.py on Python floats                                              */
+/* dtypes per family: reverse/transpose/addition/matvec/matmul take all four;
+   the Jacobi stencils take PK_DTYPE_I32.  Buffers hold elements of the dtype's size. */
 
 /*
  * One program invocation.  Parameters carry the names of the ORIGINAL
@@ -123,6 +132,15 @@ int pk_query_machine(int device, pk_machine_t *out);
  * returns after enqueueing.  Replaces interp.run_program (interp.py:215). */
 int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stream);
 
+/* pk_launch with the element count of every buffer: PK_E_BOUNDS (the
+ * reference's IndexError, interp.py:209-212) when an access of the launch
+ * would leave a buffer, before anything is enqueued. */
+int pk_launch_checked(const pk_launch_t *L, void *const *dev_ptrs, const int64_t *elems, int nptrs, void *stream);
+
+/* need[i] = 1 + the largest flat index the launch reads or writes in array i
+ * (0 if it never touches it); the stencils count their whole double buffer. */
+int pk_required_elems(const pk_launch_t *L, int64_t *need, int nneed);
+
 /* End-to-end call with HOST buffers (pass pinned memory for full PCIe
  * speed): copies the inputs in, runs pk_launch, copies the written arrays
  * back into the host buffers and synchronises.  With a unit sub-range
@@ -134,6 +152,10 @@ int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stre
  * over an H2D stream, two compute streams and a D2H stream, so the copies
  * overlap the kernels; results are identical to one pk_launch. */
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device);
+
+/* pk_run_host with element counts: PK_E_BOUNDS when a buffer is shorter than
+ * what the run touches or copies (the declared extent of each array). */
+int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device);
 
 /* One Jacobi sweep over an explicit position range, used by the slab
  * partitioner (one process per GPU).  src/dst point at the two halves (1-D:

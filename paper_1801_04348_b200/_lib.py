@@ -47,12 +47,18 @@ FLAG_NARROW = 0x20
 
 DTYPE_I32 = 0
 DTYPE_F32 = 1
+DTYPE_I64 = 2
+DTYPE_F64 = 3
+DTYPE_NAMES = {DTYPE_I32: "i32", DTYPE_F32: "f32", DTYPE_I64: "i64", DTYPE_F64: "f64"}
 
 # every symbol include/pk.h declares
 EXPORTS = (
     "pk_query_machine",
     "pk_launch",
+    "pk_launch_checked",
+    "pk_required_elems",
     "pk_run_host",
+    "pk_run_host_checked",
     "pk_launch_multi",
     "pk_jacobi_sweep",
     "pk_jacobi_sweep_peer",
@@ -159,6 +165,14 @@ def load() -> ctypes.CDLL:
         lib.pk_launch.restype = ctypes.c_int
         lib.pk_run_host.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int]
         lib.pk_run_host.restype = ctypes.c_int
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        lib.pk_launch_checked.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), i64p, ctypes.c_int, vp]
+        lib.pk_launch_checked.restype = ctypes.c_int
+        lib.pk_required_elems.argtypes = [ctypes.POINTER(PkLaunch), i64p, ctypes.c_int]
+        lib.pk_required_elems.restype = ctypes.c_int
+        lib.pk_run_host_checked.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), i64p, ctypes.c_int,
+                                            ctypes.c_int]
+        lib.pk_run_host_checked.restype = ctypes.c_int
         lib.pk_launch_multi.argtypes = [ctypes.POINTER(PkLaunch), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int64, ctypes.c_int]
         lib.pk_launch_multi.restype = ctypes.c_int
@@ -232,10 +246,28 @@ def launch(L: PkLaunch, ptrs, stream: int = 0) -> None:
     check(lib.pk_launch(ctypes.byref(L), arr, len(ptrs), ctypes.c_void_p(stream or None)))
 
 
-def run_host(L: PkLaunch, host_ptrs, device: int = 0) -> None:
+def run_host(L: PkLaunch, host_ptrs, device: int = 0, elems=None) -> None:
+    """pk_run_host (pk_run_host_checked when element counts are given)."""
     lib = load()
     arr = ptr_array(host_ptrs)
-    check(lib.pk_run_host(ctypes.byref(L), arr, len(host_ptrs), device))
+    if elems is None:
+        check(lib.pk_run_host(ctypes.byref(L), arr, len(host_ptrs), device))
+    else:
+        n = (ctypes.c_int64 * len(elems))(*[int(e) for e in elems])
+        check(lib.pk_run_host_checked(ctypes.byref(L), arr, n, len(host_ptrs), device))
+
+
+def launch_checked(L: PkLaunch, ptrs, elems, stream: int = 0) -> None:
+    lib = load()
+    n = (ctypes.c_int64 * len(elems))(*[int(e) for e in elems])
+    check(lib.pk_launch_checked(ctypes.byref(L), ptr_array(ptrs), n, len(ptrs), ctypes.c_void_p(stream or None)))
+
+
+def required_elems(L: PkLaunch, nptrs: int) -> list[int]:
+    """1 + the largest flat index the launch touches in each array (pk_required_elems)."""
+    need = (ctypes.c_int64 * 3)()
+    check(load().pk_required_elems(ctypes.byref(L), need, 3))
+    return [int(need[i]) for i in range(nptrs)]
 
 
 def launch_multi(L: PkLaunch, devices, ptr_lists, halo: int = 0, gather: bool = True) -> None:

@@ -69,5 +69,5 @@ def describe(L: _lib.PkLaunch) -> dict:
     d = L.as_dict()
     d["family"] = {v: k for k, v in _lib.FAMILY_IDS.items()}[L.family]
     d["variant"] = "direct" if L.variant == _lib.VARIANT_DIRECT else "staged"
-    d["dtype"] = "f32" if L.dtype == _lib.DTYPE_F32 else "i32"
+    d["dtype"] = _lib.DTYPE_NAMES.get(L.dtype, str(L.dtype))
     return d

@@ -5,16 +5,28 @@
 // After granularity merged the twin stores (strategies.py:213-262) the program
 // reads dim1 = N/B1 and covers j < dim1*B1 with one store; that variant is
 // selected with PK_FLAG_MERGED when the caller runs the rewritten program.
-// HBM-bound: 12 bytes per written element.
+// HBM-bound: 3 * sizeof(element) bytes per written element.  Element types:
+// int32 / int64 wrap like C (exact whenever the sum fits; the Python shim
+// picks int64 when int32 might not hold the reference's unbounded sum),
+// float32 / binary64 add with one IEEE rounding -- binary64 is the
+// reference's Python float addition, bit for bit.
 #include "pk_internal.cuh"
 
 namespace pk {
 namespace {
 
 // One block row-strip: rows [r0, r0+rows), columns of the covered ranges
-// [0, J) and, for the twin form, [half, half+J).  int32 wraps like C int.
-__global__ void __launch_bounds__(256) k_addition(const int *__restrict__ a, const int *__restrict__ b,
-                                                 int *__restrict__ c, int64_t N, int64_t rlo,
+// [0, J) and, for the twin form, [half, half+J).
+__device__ __forceinline__ int add_elem(int x, int y) { return (int)((unsigned)x + (unsigned)y); }
+__device__ __forceinline__ long long add_elem(long long x, long long y) {
+    return (long long)((unsigned long long)x + (unsigned long long)y);
+}
+__device__ __forceinline__ float add_elem(float x, float y) { return __fadd_rn(x, y); }
+__device__ __forceinline__ double add_elem(double x, double y) { return __dadd_rn(x, y); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_addition(const T *__restrict__ a, const T *__restrict__ b,
+                                                 T *__restrict__ c, int64_t N, int64_t rlo,
                                                  int64_t rhi, int64_t J, int64_t half, int twin,
                                                  int rows_per_block) {
     const int64_t r0 = rlo + (int64_t)blockIdx.y * rows_per_block;
@@ -25,9 +37,23 @@ __global__ void __launch_bounds__(256) k_addition(const int *__restrict__ a, con
         for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < span;
              e += (int64_t)gridDim.x * blockDim.x) {
             const int64_t j = e < J ? e : half + (e - J);
-            c[row + j] = (int)((unsigned)a[row + j] + (unsigned)b[row + j]);
+            c[row + j] = add_elem(a[row + j], b[row + j]);
         }
     }
+}
+
+template <typename T>
+void launch_t(void *const *p, int64_t N, int64_t rlo, int64_t rhi, int64_t J, int64_t half, bool merged,
+              int64_t span, cudaStream_t st) {
+    const int nt = 256;
+    int64_t gx = ceil_div(span, nt);
+    if (gx > 4096) gx = 4096;
+    int rows_per_block = 8;
+    if (ceil_div(rhi - rlo, rows_per_block) > 65535) rows_per_block = (int)ceil_div(rhi - rlo, 65535);  // fold rows
+    const int64_t gy = ceil_div(rhi - rlo, rows_per_block);
+    k_addition<T><<<dim3((unsigned)gx, (unsigned)gy), nt, 0, st>>>(
+        static_cast<const T *>(p[0]), static_cast<const T *>(p[1]), static_cast<T *>(p[2]), N, rlo, rhi, J, half,
+        merged ? 0 : 1, rows_per_block);
 }
 
 }  // namespace
@@ -49,21 +75,12 @@ int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     unit_range(L, 0, I, &rlo, &rhi);
     if (rhi <= rlo || J <= 0) return PK_OK;
     const int64_t span = merged ? J : 2 * J;
-    const int nt = 256;
-    int64_t gx = ceil_div(span, nt);
-    if (gx > 4096) gx = 4096;
-    const int rows_per_block = 8;
-    const int64_t gy = ceil_div(rhi - rlo, rows_per_block);
-    if (gy > 65535) {
-        // fold extra rows into each block
-        const int64_t rpb = ceil_div(rhi - rlo, 65535);
-        k_addition<<<dim3((unsigned)gx, (unsigned)ceil_div(rhi - rlo, rpb)), nt, 0, st>>>(
-            static_cast<const int *>(p[0]), static_cast<const int *>(p[1]), static_cast<int *>(p[2]),
-            L.N, rlo, rhi, J, half, merged ? 0 : 1, (int)rpb);
-    } else {
-        k_addition<<<dim3((unsigned)gx, (unsigned)gy), nt, 0, st>>>(
-            static_cast<const int *>(p[0]), static_cast<const int *>(p[1]), static_cast<int *>(p[2]),
-            L.N, rlo, rhi, J, half, merged ? 0 : 1, rows_per_block);
+    switch (L.dtype) {
+        case PK_DTYPE_I32: launch_t<int>(p, L.N, rlo, rhi, J, half, merged, span, st); break;
+        case PK_DTYPE_F32: launch_t<float>(p, L.N, rlo, rhi, J, half, merged, span, st); break;
+        case PK_DTYPE_I64: launch_t<long long>(p, L.N, rlo, rhi, J, half, merged, span, st); break;
+        case PK_DTYPE_F64: launch_t<double>(p, L.N, rlo, rhi, J, half, merged, span, st); break;
+        default: return fail(PK_E_UNSUPPORTED, "addition: dtype %d", L.dtype);
     }
     return after_launch("addition");
 }

@@ -30,6 +30,12 @@ namespace {
 
 __device__ __forceinline__ float mad(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ int mad(int a, int b, int c) { return a * b + c; }
+// int64 wraps like C (exact modulo 2^64); binary64 rounds the product and the
+// sum separately, c + a*b exactly as the interpreter evaluates Python floats
+__device__ __forceinline__ long long mad(long long a, long long b, long long c) {
+    return (long long)((unsigned long long)a * (unsigned long long)b + (unsigned long long)c);
+}
+__device__ __forceinline__ double mad(double a, double b, double c) { return __dadd_rn(c, __dmul_rn(a, b)); }
 
 constexpr int kChunk = 8;  // accumulators per thread in the generic kernel
 
@@ -256,13 +262,15 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
             matmul_tma_fits(L.B0, L.ub1 * elems(L), rhi - rlo, Nc, K, L.N) && rlo % 4 == 0)
             return launch_matmul_tma(a, b, c, L.N, rlo, rhi, Nc, K, st);
     }
-    if (L.variant == PK_VARIANT_STAGED && !generic && L.N % 4 == 0 && K % 16 == 0 &&
-        aligned16(a) && aligned16(b) && aligned16(c) && (rhi - rlo) % BM == 0 && Nc % BN == 0 &&
-        rlo % 4 == 0) {
-        if (BM == 128 && BN == 128) return launch_tiled<T, 16, 16, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
-        if (BM == 64 && BN == 128) return launch_tiled<T, 8, 16, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
-        if (BM == 128 && BN == 64) return launch_tiled<T, 16, 8, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
-        if (BM == 64 && BN == 64) return launch_tiled<T, 8, 8, 16>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+    if constexpr (sizeof(T) == 4) {
+        if (L.variant == PK_VARIANT_STAGED && !generic && L.N % 4 == 0 && K % 16 == 0 &&
+            aligned16(a) && aligned16(b) && aligned16(c) && (rhi - rlo) % BM == 0 && Nc % BN == 0 &&
+            rlo % 4 == 0) {
+            if (BM == 128 && BN == 128) return launch_tiled<T, 16, 16, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+            if (BM == 64 && BN == 128) return launch_tiled<T, 8, 16, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+            if (BM == 128 && BN == 64) return launch_tiled<T, 16, 8, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+            if (BM == 64 && BN == 64) return launch_tiled<T, 8, 8, 16>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+        }
     }
     if (L.B0 * L.ub1 > 1024)
         return fail(PK_E_PARAM, "matmul: thread block B0*ub1 = %lld exceeds 1024 (T_B)",
@@ -300,6 +308,8 @@ int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     if (rhi <= rlo || Nc <= 0) return PK_OK;
     if (L.dtype == PK_DTYPE_F32) return launch_t<float>(L, p, st, rlo, rhi, Nc, K);
     if (L.dtype == PK_DTYPE_I32) return launch_t<int>(L, p, st, rlo, rhi, Nc, K);
+    if (L.dtype == PK_DTYPE_F64) return launch_t<double>(L, p, st, rlo, rhi, Nc, K);
+    if (L.dtype == PK_DTYPE_I64) return launch_t<long long>(L, p, st, rlo, rhi, Nc, K);
     return fail(PK_E_UNSUPPORTED, "matmul: dtype %d", L.dtype);
 }
 

@@ -206,6 +206,54 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
     return after_launch("matvec");
 }
 
+// int64 and binary64: one thread per row in the interpreter's own order,
+// acc = y[r]; acc = acc + a[r][q]*x[q] for q ascending, one rounding per
+// operation (no contraction) -- bit-identical to interp.py on Python floats;
+// int64 wraps like C (exact modulo 2^64, so exact whenever the result fits).
+// A block owns 128 rows; 32-column tiles of a are loaded row-coalesced (each
+// warp reads one 256-byte row segment per step) into a transposed shared
+// tile, so every thread then walks its own row's columns.
+__device__ __forceinline__ double madd(double acc, double a, double x) { return __dadd_rn(acc, __dmul_rn(a, x)); }
+__device__ __forceinline__ long long madd(long long acc, long long a, long long x) {
+    return (long long)((unsigned long long)acc + (unsigned long long)a * (unsigned long long)x);
+}
+
+constexpr int kExactRows = 128, kExactCols = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kExactRows) k_matvec_exact(const T *__restrict__ a, const T *__restrict__ x,
+                                                            T *__restrict__ y, int64_t N, int64_t rlo, int64_t rhi) {
+    __shared__ T tile[kExactCols][kExactRows + 1];
+    __shared__ T xs[kExactCols];
+    const int64_t r0 = rlo + (int64_t)blockIdx.x * kExactRows;
+    const int t = threadIdx.x;
+    const bool live = r0 + t < rhi;
+    const int nrows = (int)min((int64_t)kExactRows, rhi - r0);
+    T acc = live ? y[r0 + t] : T(0);
+    for (int64_t q0 = 0; q0 < N; q0 += kExactCols) {
+        const int nc = (int)min((int64_t)kExactCols, N - q0);
+        for (int e = t; e < kExactRows * kExactCols; e += kExactRows) {
+            const int rr = e / kExactCols, cc = e % kExactCols;
+            tile[cc][rr] = (rr < nrows && cc < nc) ? a[(r0 + rr) * N + q0 + cc] : T(0);
+        }
+        if (t < kExactCols) xs[t] = t < nc ? x[q0 + t] : T(0);
+        __syncthreads();
+        for (int cc = 0; cc < nc; cc++) acc = madd(acc, tile[cc][t], xs[cc]);
+        __syncthreads();
+    }
+    if (live) y[r0 + t] = acc;
+}
+
+template <typename T>
+int launch_exact(void *const *p, int64_t N, int64_t rlo, int64_t rhi, cudaStream_t st) {
+    const int64_t blocks = ceil_div(rhi - rlo, kExactRows);
+    if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matvec: grid too large");
+    k_matvec_exact<T><<<(unsigned)blocks, kExactRows, 0, st>>>(static_cast<const T *>(p[0]),
+                                                               static_cast<const T *>(p[1]),
+                                                               static_cast<T *>(p[2]), N, rlo, rhi);
+    return after_launch("matvec_exact");
+}
+
 }  // namespace
 
 int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st) {
@@ -217,6 +265,8 @@ int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     if (rhi <= rlo) return PK_OK;
     if (L.dtype == PK_DTYPE_I32) return launch_t<int>(L, p, st, rlo, rhi);
     if (L.dtype == PK_DTYPE_F32) return launch_t<float>(L, p, st, rlo, rhi);
+    if (L.dtype == PK_DTYPE_F64) return launch_exact<double>(p, L.N, rlo, rhi, st);
+    if (L.dtype == PK_DTYPE_I64) return launch_exact<long long>(p, L.N, rlo, rhi, st);
     return fail(PK_E_UNSUPPORTED, "matvec: dtype %d", L.dtype);
 }
 

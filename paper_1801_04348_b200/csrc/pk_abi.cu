@@ -127,6 +127,73 @@ void array_range(const pk_launch_t &L, int i, int64_t elems, int64_t *off, int64
     *cnt = b > a ? b - a : 0;
 }
 
+// Elements of each array a launch touches: 1 + the largest flat index it
+// reads or writes over its covered index sets (the reference raises
+// IndexError for any access past the end, interp.py:209-212), 0 for an
+// array it never touches.  The stencils count their whole double buffer
+// (their value-range pre-pass reads it).
+int required_elems(const pk_launch_t &L, int64_t need[3]) {
+    need[0] = need[1] = need[2] = 0;
+    const int64_t N = L.N;
+    if (N <= 0) return PK_OK;
+    int64_t lo, hi;
+    switch (L.family) {
+        case PK_FAMILY_REVERSE: {
+            if (L.s * L.B == 0) return fail(PK_E_DIV0, "reverse: s*B == 0 in dim = N / (s * B)");
+            if (L.s < 0 || L.B < 0) return PK_OK;
+            unit_range(L, 0, max0(N / (L.s * L.B)) * L.s * L.B, &lo, &hi);
+            if (hi > lo) need[0] = hi, need[1] = N - lo;
+            return PK_OK;
+        }
+        case PK_FAMILY_TRANSPOSE: {
+            if (L.B0 == 0 || L.s * L.B1 == 0) return fail(PK_E_DIV0, "transpose: zero divisor in dim0 / dim1");
+            if (L.B0 < 0 || L.B1 < 0 || L.s < 0) return PK_OK;
+            const int64_t J = max0(N / (L.s * L.B1)) * L.s * L.B1;
+            unit_range(L, 0, max0(N / L.B0) * L.B0, &lo, &hi);
+            if (hi > lo && J > 0) need[0] = (J - 1) * N + hi, need[1] = (hi - 1) * N + J;
+            return PK_OK;
+        }
+        case PK_FAMILY_JACOBI1D:
+        case PK_FAMILY_JACOBI2D: {
+            const bool two = L.family == PK_FAMILY_JACOBI2D;
+            const int64_t tile = two ? L.B0 : L.s * L.B;
+            if (tile == 0 || (two && L.s * L.B1 == 0)) return fail(PK_E_DIV0, "jacobi: zero divisor in dim");
+            if (L.T <= 0 || L.s < 0 || L.B < 0 || L.B0 < 0 || L.B1 < 0) return PK_OK;
+            const int64_t P = max0((N - 2) / tile) * tile;
+            const int64_t J = two ? max0((N - 2) / (L.s * L.B1)) * L.s * L.B1 : 1;
+            if (P > 0 && J > 0) need[0] = two ? 2 * N * N : 2 * N;
+            return PK_OK;
+        }
+        case PK_FAMILY_MATVEC: {
+            if (L.s * L.B == 0) return fail(PK_E_DIV0, "matvec: s*B == 0 in dim = N / (s * B)");
+            if (L.s < 0 || L.B < 0) return PK_OK;
+            unit_range(L, 0, max0(N / (L.s * L.B)) * L.s * L.B, &lo, &hi);
+            if (hi > lo) need[0] = hi * N, need[1] = N, need[2] = hi;
+            return PK_OK;
+        }
+        case PK_FAMILY_MATMUL: {
+            if (L.B0 == 0 || L.ub1 * L.s == 0) return fail(PK_E_DIV0, "matmul: zero divisor in dim0 / dim1");
+            if (L.B0 < 0 || L.ub1 < 0 || L.s < 0) return PK_OK;
+            const int64_t K = max0(N / L.B0) * L.B0, Nc = max0(N / (L.ub1 * L.s)) * L.ub1 * L.s;
+            unit_range(L, 0, K, &lo, &hi);  // rows p < dim0*B0 == kdim*B0
+            if (hi > lo && Nc > 0 && K > 0)
+                need[0] = (hi - 1) * N + K, need[1] = (K - 1) * N + Nc, need[2] = (hi - 1) * N + Nc;
+            return PK_OK;
+        }
+        case PK_FAMILY_ADDITION: {
+            const bool merged = (L.flags & PK_FLAG_MERGED) != 0;
+            if (L.B0 == 0 || L.B1 == 0) return fail(PK_E_DIV0, "addition: zero divisor in dim0 / dim1");
+            if (L.B0 < 0 || L.B1 < 0) return PK_OK;
+            int64_t J = merged ? max0(N / L.B1) * L.B1 : max0(N / (2 * L.B1)) * L.B1;
+            if (!merged && J > N / 2) J = N / 2;
+            unit_range(L, 0, max0(N / L.B0) * L.B0, &lo, &hi);
+            if (hi > lo && J > 0) need[0] = need[1] = need[2] = (hi - 1) * N + (merged ? J : N / 2 + J);
+            return PK_OK;
+        }
+        default: return fail(PK_E_UNSUPPORTED, "unknown program family %d", L.family);
+    }
+}
+
 int dispatch(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     switch (L.family) {
         case PK_FAMILY_REVERSE: return launch_reverse(L, p, st);
@@ -149,9 +216,8 @@ int validate(const pk_launch_t *L, int nptrs) {
         return fail(PK_E_PARAM, "family %d takes %d arrays, got %d", L->family, s.count, nptrs);
     if (L->variant != PK_VARIANT_STAGED && L->variant != PK_VARIANT_DIRECT)
         return fail(PK_E_UNSUPPORTED, "unknown variant %d", L->variant);
-    const bool fp_ok = L->family == PK_FAMILY_MATMUL || L->family == PK_FAMILY_MATVEC ||
-                       L->family == PK_FAMILY_TRANSPOSE || L->family == PK_FAMILY_REVERSE;
-    if (L->dtype != PK_DTYPE_I32 && !(L->dtype == PK_DTYPE_F32 && fp_ok))
+    const bool stencil = L->family == PK_FAMILY_JACOBI1D || L->family == PK_FAMILY_JACOBI2D;
+    if (L->dtype < PK_DTYPE_I32 || L->dtype > PK_DTYPE_F64 || (stencil && L->dtype != PK_DTYPE_I32))
         return fail(PK_E_UNSUPPORTED, "dtype %d not provided for family %d", L->dtype, L->family);
     if ((L->flags & PK_FLAG_TF32X3) && !(L->family == PK_FAMILY_MATMUL && L->dtype == PK_DTYPE_F32))
         return fail(PK_E_UNSUPPORTED, "3xTF32 applies to float32 matmul only");
@@ -167,7 +233,7 @@ using namespace pk;
 
 extern "C" {
 
-int pk_version(void) { return (1 << 16) | 1; }  // 1.1: pk_jacobi_sweep_peer, pk_ipc_*
+int pk_version(void) { return (1 << 16) | 2; }  // 1.2: 8-byte dtypes, pk_launch_checked, pk_required_elems
 
 const char *pk_last_error(void) { return t_err; }
 
@@ -213,6 +279,35 @@ int pk_launch(const pk_launch_t *L, void *const *dev_ptrs, int nptrs, void *stre
     for (int i = 0; i < nptrs; i++)
         if (!dev_ptrs || !dev_ptrs[i]) return fail(PK_E_PARAM, "array %d is a null pointer", i);
     return dispatch(*L, dev_ptrs, static_cast<cudaStream_t>(stream));
+}
+
+int pk_required_elems(const pk_launch_t *L, int64_t *need, int nneed) {
+    if (!L || !need) return fail(PK_E_PARAM, "null argument");
+    ArraySpec s;
+    int rc = array_spec(*L, &s);
+    if (rc) return rc;
+    if (nneed < s.count) return fail(PK_E_PARAM, "family %d has %d arrays, room for %d", L->family, s.count, nneed);
+    int64_t n[3];
+    rc = required_elems(*L, n);
+    if (rc) return rc;
+    for (int i = 0; i < s.count; i++) need[i] = n[i];
+    return PK_OK;
+}
+
+int pk_launch_checked(const pk_launch_t *L, void *const *dev_ptrs, const int64_t *elems, int nptrs, void *stream) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    if (!elems) return fail(PK_E_PARAM, "null element counts");
+    int64_t need[3];
+    rc = required_elems(*L, need);
+    if (rc) return rc;
+    static const char *names[7][3] = {{"a", "c", ""}, {"a", "c", ""}, {"a", "", ""}, {"a", "", ""},
+                                      {"a", "x", "y"}, {"a", "b", "c"}, {"a", "b", "c"}};
+    for (int i = 0; i < nptrs; i++)
+        if (elems[i] < need[i])
+            return fail(PK_E_BOUNDS, "access %s[%lld] out of bounds (size %lld)", names[L->family - 1][i],
+                        (long long)(need[i] - 1), (long long)elems[i]);
+    return pk_launch(L, dev_ptrs, nptrs, stream);
 }
 
 int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
@@ -372,6 +467,25 @@ void host_run_release(HostRun &R, bool healthy) {
 
 }  // namespace
 
+int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    if (!elems) return fail(PK_E_PARAM, "null element counts");
+    int64_t need[3];
+    rc = required_elems(*L, need);
+    if (rc) return rc;
+    ArraySpec spec;
+    array_spec(*L, &spec);
+    for (int i = 0; i < nptrs; i++) {
+        // pk_run_host moves the declared extent of every array it is given
+        const int64_t want = host_ptrs && host_ptrs[i] ? spec.elems[i] : 0;
+        if (elems[i] < need[i] || elems[i] < want)
+            return fail(PK_E_BOUNDS, "array %d: %lld elements, the run touches %lld and copies %lld", i,
+                        (long long)elems[i], (long long)need[i], (long long)want);
+    }
+    return pk_run_host(L, host_ptrs, nptrs, device);
+}
+
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device) {
     int rc = validate(L, nptrs);
     if (rc) return rc;
@@ -387,8 +501,9 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     // whole (matmul's b, mat-vec's x, transpose's a) go up once, first.
     const int64_t N = L->N > 0 ? L->N : 0;
     const int64_t u0 = L->hi > 0 ? (L->lo > 0 ? L->lo : 0) : 0, u1 = L->hi > 0 ? L->hi : N;
+    const int64_t eb = elem_bytes(*L);  // bytes per element
     int64_t unit_bytes = 0;  // streamed bytes per unit
-    for (int i = 0; i < spec.count; i++) unit_bytes += (spec.written[i] ? 2 : 1) * (spec.elems[i] / (N > 0 ? N : 1)) * 4;
+    for (int i = 0; i < spec.count; i++) unit_bytes += (spec.written[i] ? 2 : 1) * (spec.elems[i] / (N > 0 ? N : 1)) * eb;
     int nchunks = 1;
     if (chunkable(*L) && u1 > u0 && unit_bytes > 0) {
         const int64_t total = (u1 - u0) * unit_bytes;
@@ -424,7 +539,7 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     };
     bool whole[3] = {false, false, false};  // needed whole by every chunk: moved once
     for (int i = 0; i < spec.count && rc == PK_OK; i++) {
-        const size_t bytes = (size_t)spec.elems[i] * 4;
+        const size_t bytes = (size_t)spec.elems[i] * eb;
         e = scratch_alloc(&R.dev[i], bytes, R.h2d);
         if (e != cudaSuccess) {
             rc = fail(PK_E_ALLOC, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
@@ -448,13 +563,13 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         if (slice < 0) slice = 0;
     }
     auto up_range = [&](int i, int64_t off, int64_t cnt) -> int {
-        char *d = static_cast<char *>(R.dev[i]) + off * 4;
+        char *d = static_cast<char *>(R.dev[i]) + off * eb;
         if (cnt && host_ptrs[i]) {
-            cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * 4, (size_t)cnt * 4,
+            cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * eb, (size_t)cnt * eb,
                                             cudaMemcpyHostToDevice, R.h2d);
             if (x != cudaSuccess) return fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(x));
         } else if (cnt) {
-            cudaMemsetAsync(d, 0, (size_t)cnt * 4, R.h2d);  // missing arrays are zero-filled (interp.py:79-81)
+            cudaMemsetAsync(d, 0, (size_t)cnt * eb, R.h2d);  // missing arrays are zero-filled (interp.py:79-81)
         }
         return PK_OK;
     };
@@ -467,8 +582,8 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         int64_t off, cnt;
         array_range(C, i, spec.elems[i], &off, &cnt);
         if (!spec.written[i] || !cnt || !host_ptrs[i]) return PK_OK;
-        cudaError_t x = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * 4,
-                                        static_cast<char *>(R.dev[i]) + off * 4, (size_t)cnt * 4,
+        cudaError_t x = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * eb,
+                                        static_cast<char *>(R.dev[i]) + off * eb, (size_t)cnt * eb,
                                         cudaMemcpyDeviceToHost, R.d2h);
         return x == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(x));
     };
@@ -711,6 +826,7 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         if (rc || !gather) return finish(rc);
         ArraySpec spec;
         array_spec(*L, &spec);
+        const int64_t eb = elem_bytes(*L);
         cudaSetDevice(devices[0]);
         for (int k = 1; k < ndev && rc == PK_OK; k++) {
             if (Ls[k].hi <= Ls[k].lo) continue;
@@ -719,8 +835,8 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
                 if (!spec.written[i]) continue;
                 int64_t off, cnt;
                 array_range(Ls[k], i, spec.elems[i], &off, &cnt);
-                rc = peer_copy(static_cast<char *>(ptrs(0)[i]) + off * 4, devices[0],
-                               static_cast<const char *>(ptrs(k)[i]) + off * 4, devices[k], (size_t)cnt * 4, M.st[0]);
+                rc = peer_copy(static_cast<char *>(ptrs(0)[i]) + off * eb, devices[0],
+                               static_cast<const char *>(ptrs(k)[i]) + off * eb, devices[k], (size_t)cnt * eb, M.st[0]);
             }
         }
         return finish(rc);

@@ -146,6 +146,11 @@ int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);
 // Shared-memory words staged per block (0 for direct variants).
 int64_t footprint_words(const pk_launch_t &L);
 
+// Bytes per array element of a launch (PK_DTYPE_*).
+inline int elem_bytes(const pk_launch_t &L) {
+    return (L.dtype == PK_DTYPE_I64 || L.dtype == PK_DTYPE_F64) ? 8 : 4;
+}
+
 // Elements per thread along the s axis: 1 once granularity removed the loop.
 inline int64_t elems(const pk_launch_t &L) {
     return (L.flags & PK_FLAG_GRANULARITY) ? 1 : L.s;

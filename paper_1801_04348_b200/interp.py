@@ -24,11 +24,12 @@ on the caller's device buffers without copies.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib, binding, cases
+from . import _lib, binding, cases, marshal
 from .programs import FAMILIES, effective_params, identify
 
 _INT32_MIN, _INT32_MAX = -(2**31), 2**31 - 1
@@ -153,6 +154,37 @@ def _shapes_py(fam, P):
     return out
 
 
+class _PinnedPool:
+    """Page-locked staging buffers for the host-array path, kept across calls
+    (pinning is slow; pk_run_host needs pinned memory to overlap its PCIe
+    copies with the kernels).  One set per declared-array slot, grown on
+    demand; a lock serialises callers (each call holds its buffers until the
+    results are copied out)."""
+
+    def __init__(self):
+        import threading
+
+        self.lock = threading.Lock()
+        self.bufs: dict[int, object] = {}
+
+    def view(self, slot: int, count: int, dtype) -> np.ndarray:
+        torch = _torch()
+        nbytes = max(count, 1) * np.dtype(dtype).itemsize
+        buf = self.bufs.get(slot)
+        if buf is None or buf.numel() < nbytes:
+            cap = 1 << max(20, (nbytes - 1).bit_length())  # powers of two, >= 1 MiB
+            self.bufs[slot] = None
+            buf = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            self.bufs[slot] = buf
+        return buf.numpy()[:nbytes].view(dtype)
+
+    def release(self) -> None:
+        self.bufs.clear()
+
+
+_pinned = _PinnedPool()
+
+
 def run_program(
     program,
     params: dict,
@@ -170,6 +202,17 @@ def run_program(
     halo: int = 0,
 ) -> dict:
     """Execute the whole program on the GPU; returns the final array contents.
+
+    Values keep the reference's semantics (marshal.py): Python floats and
+    float64 data compute in binary64 with the interpreter's rounding
+    sequence, float32 data on the float32 path (FFMA matmul, BASELINE
+    configs[0-1]), ints exactly (int32 or int64 words, ``OverflowError``
+    beyond int64); reverse / transpose return the very objects they moved.
+
+    Host arrays (lists, numpy, CPU tensors) go through ``pk_run_host`` from
+    pooled pinned buffers: uploads, kernels and downloads overlap.  CUDA
+    tensors stay on their device (``inplace=True`` runs on them without a
+    copy).
 
     ``machine``: the machine values for case selection (default: the live
     device).  ``case``: force a leaf by index (tests / tuner).  ``generic``:
@@ -196,9 +239,15 @@ def run_program(
             raise
         from . import jit
 
+        warnings.warn("program matches none of the seven kernel families: running the reference emitter's "
+                      "leaf compiled with NVRTC (no hand-written kernel)", RuntimeWarning, stacklevel=2)
         leaf = jit.emit_leaf(program, params)
         _last = RunInfo("emitted", None, tuple(leaf.applied), False, {"kernel": leaf.kernel_name}, 0)
         return jit.run_program_jit(leaf, params, arrays)
+    rename = getattr(kind, "rename", None) or {}
+    if rename:  # an alpha-renamed copy of a known program: speak the family's names inside
+        params = {rename.get(k, k): v for k, v in params.items()}
+        arrays = {rename.get(k, k): v for k, v in (arrays or {}).items()}
     P = effective_params(kind, params)
     fam = FAMILIES[kind.family]
     torch = _torch()
@@ -210,11 +259,15 @@ def run_program(
             raise ValueError("devices must name at least one GPU")
         device = devices[0]
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-    mv = None
+
+    arrays = dict(arrays or {})  # arrays the program does not declare come back as copies (below)
+    declared = [a.name for a in fam.arrays]
+    plan, srcs = marshal.plan(kind.family, P, {n: arrays[n] for n in declared if n in arrays})
+
     if machine is None or machine == "live":
         from . import machine as machine_mod
 
-        mv = machine_mod.live(dev.index)
+        mv = machine_mod.live(dev.index, elem_bytes=plan.elem_bytes)
     else:
         mv = machine
 
@@ -232,54 +285,65 @@ def run_program(
     else:
         applied, case_index, fallback = kind.applied, None, False
 
-    arrays = dict(arrays or {})  # arrays the program does not declare come back as copies (below)
-    dtypes = {_dtype_of(v) for n, v in arrays.items() if n in {a.name for a in fam.arrays}}
-    if "f" in dtypes:
-        if not fam.float_ok:
-            raise NotImplementedError("%s computes on C ints; float arrays are not supported" % kind.family)
-        np_dtype, dtype = np.float32, _lib.DTYPE_F32
-    else:
-        np_dtype, dtype = np.int32, _lib.DTYPE_I32
-
     shapes = _shapes_py(fam, P)
-    kinds = [_kind_of(v) for v in arrays.values()]
+    counts = {n: _numel(shapes[n]) for n in declared}
+    kinds = [marshal.kind_of(v) for v in arrays.values()]
     default_kind = kinds[0] if kinds else "list"
 
-    L = binding.make_launch(kind, P, applied, dtype, generic=generic,
+    L = binding.make_launch(kind, P, applied, plan.dtype, generic=generic,
                             extra_flags=(_lib.FLAG_TF32X3 if tf32x3 else 0) | (_lib.FLAG_TEMPORAL if temporal else 0))
     if temporal:
         L.tblock = int(temporal)  # steps fused per HBM pass (odd; Jacobi programs only)
-    stream = torch.cuda.current_stream(dev).cuda_stream
-
-    with torch.cuda.device(dev):
-        bufs, sizes, owned = [], {}, {}
-        for a in fam.arrays:
-            shape = shapes[a.name]
-            want = _numel(shape)
-            if a.name in arrays:
-                v = arrays[a.name]
-                if (inplace and _kind_of(v) == "torch" and v.is_cuda and v.is_contiguous()
-                        and v.dtype == (torch.float32 if dtype == _lib.DTYPE_F32 else torch.int32)):
+    # IndexError exactly where an access of the run would leave a supplied array
+    need = _lib.required_elems(L, len(declared))
+    for i, n in enumerate(declared):
+        if n in srcs and srcs[n].size < need[i]:
+            raise IndexError("access %s[%d] out of bounds (size %d)" % (n, need[i] - 1, srcs[n].size))
+    runnable = all(counts[n] > 0 for n in declared)
+    on_device = any(s.kind == "torch" and s.value.is_cuda for s in srcs.values())
+    multi = devices is not None and len(devices) > 1
+    words = {}
+    if not on_device and not multi and not inplace:
+        # host arrays: pinned staging + pk_run_host (copies overlap the kernels)
+        with _pinned.lock:
+            bufs = []
+            for i, n in enumerate(declared):
+                buf = _pinned.view(i, counts[n], plan.np_dtype)
+                marshal.host_words(plan, srcs.get(n), counts[n], buf)
+                bufs.append(buf)
+            if runnable:
+                with torch.cuda.device(dev):
+                    _lib.run_host(L, [b.ctypes.data for b in bufs], dev.index, elems=[counts[n] for n in declared])
+            for n, buf in zip(declared, bufs):
+                words[n] = buf[: counts[n]].copy()
+    else:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        with torch.cuda.device(dev):
+            bufs = []
+            for n in declared:
+                v = arrays.get(n)
+                if (inplace and v is not None and marshal.kind_of(v) == "torch" and v.is_cuda and v.is_contiguous()
+                        and not plan.objects and v.dtype == marshal.torch_dtype(plan)):
                     t = v.reshape(-1)
-                    sizes[a.name] = t.numel()
+                elif n in srcs:
+                    t = marshal.device_words(plan, srcs[n], counts[n], dev)
+                elif plan.objects:
+                    t = torch.full((max(counts[n], 1),), plan.zero_index, dtype=torch.int64, device=dev)
                 else:
-                    t, sizes[a.name] = _to_device_tensor(a.name, v, shape, np_dtype, dev)
-            else:
-                t = torch.zeros(max(want, 1), dtype=torch.float32 if dtype == _lib.DTYPE_F32 else torch.int32,
-                                device=dev)
-                sizes[a.name] = want
-            owned[a.name] = t
-            bufs.append(t)
-        if all(_numel(shapes[a.name]) > 0 for a in fam.arrays):
-            if devices is not None and len(devices) > 1:
-                # inputs replicated on every device (full-size arrays, global indexing)
-                reps = [bufs] + [[b.to(torch.device("cuda", d), copy=True) for b in bufs] for d in devices[1:]]
-                for d in set(devices):
-                    torch.cuda.synchronize(d)
-                _lib.launch_multi(L, devices, [[b.data_ptr() for b in r] for r in reps], halo=halo)
-            else:
-                _lib.launch(L, [b.data_ptr() for b in bufs], stream)
-        torch.cuda.current_stream(dev).synchronize()
+                    t = torch.zeros(max(counts[n], 1), dtype=marshal.torch_dtype(plan), device=dev)
+                bufs.append(t)
+            if runnable:
+                if multi:
+                    # inputs replicated on every device (full-size arrays, global indexing)
+                    reps = [bufs] + [[b.to(torch.device("cuda", d), copy=True) for b in bufs] for d in devices[1:]]
+                    for d in set(devices):
+                        torch.cuda.synchronize(d)
+                    _lib.launch_multi(L, devices, [[b.data_ptr() for b in r] for r in reps], halo=halo)
+                else:
+                    _lib.launch_checked(L, [b.data_ptr() for b in bufs], [b.numel() for b in bufs], stream)
+            torch.cuda.current_stream(dev).synchronize()
+        for n, t in zip(declared, bufs):
+            words[n] = t
 
     _last = RunInfo(kind.family, case_index, tuple(applied), fallback, binding.describe(L),
                     _lib.footprint_words(L))
@@ -287,21 +351,19 @@ def run_program(
     out = {}
     # arrays the caller passed that the program does not declare come back as copies
     for name, v in arrays.items():
-        if name not in owned:
+        if name not in counts:
             out[name] = _deep_copy(v)
-    for a in fam.arrays:
-        shape = shapes[a.name]
-        like = arrays.get(a.name)
-        k = _kind_of(like) if like is not None else default_kind
-        t = owned[a.name]
-        if inplace and like is not None and _kind_of(like) == "torch" and like.is_cuda and t.data_ptr() == like.data_ptr():
-            out[a.name] = like
+    for n in declared:
+        like = arrays.get(n)
+        if (inplace and like is not None and marshal.kind_of(like) == "torch" and like.is_cuda
+                and words[n].data_ptr() == like.data_ptr()):
+            out[n] = like
             continue
-        if sizes[a.name] != _numel(shape):
-            t = t[: sizes[a.name]]
-            out[a.name] = _from_device(t, k, (sizes[a.name],), like)
-        else:
-            out[a.name] = _from_device(t[: _numel(shape)], k, shape, like)
+        k = marshal.kind_of(like) if like is not None else default_kind
+        out[n] = marshal.finish(plan, srcs.get(n), words[n], shapes[n], k, like)
+    if rename:
+        back = {v: k for k, v in rename.items()}
+        out = {back.get(k, k): v for k, v in out.items()}
     return out
 
 

@@ -59,10 +59,14 @@ class MachineValues:
     warp_size: int = 32
 
 
-def values_from_props(props: dict, smem: str = "optin") -> dict:
+def values_from_props(props: dict, smem: str = "optin", elem_bytes: int = 4) -> dict:
+    """Machine values of the case discussion.  Z_B counts shared-memory
+    words of the program's element type: the footprints (counters.py:416-464)
+    count array elements, so 8-byte elements (int64 / binary64 data) see half
+    as many."""
     smem_bytes = props["smem_per_block_optin"] if smem == "optin" else props["smem_per_block"]
     return {
-        "Z_B": int(smem_bytes) // 4,
+        "Z_B": int(smem_bytes) // int(elem_bytes),
         "R_B": int(props["regs_per_thread"]),
         "T_B": int(props["max_threads_per_block"]),
     }
@@ -83,16 +87,17 @@ def _with_occupancy(mv: MachineValues, occupancy) -> MachineValues:
     return MachineValues("b200-occ", values, mv.source, mv.props, mv.warp_size)
 
 
-def live(device: int = 0, smem: str = "optin", occupancy=None) -> MachineValues:
+def live(device: int = 0, smem: str = "optin", occupancy=None, elem_bytes: int = 4) -> MachineValues:
     """Query the device (pk_query_machine) -- replaces the machine constants.
-    ``occupancy``: evaluate the occupancy model with this target O."""
+    ``occupancy``: evaluate the occupancy model with this target O.
+    ``elem_bytes``: size of the program's array elements (Z_B in elements)."""
     props = dict(_live_props(device))
     if props.get("cc_major") != 10:
         raise RuntimeError(
             "device %d is sm_%d%d; libpk is built for sm_100a only"
             % (device, props.get("cc_major"), props.get("cc_minor"))
         )
-    mv = MachineValues("b200", values_from_props(props, smem), "live:%d" % device, props,
+    mv = MachineValues("b200", values_from_props(props, smem, elem_bytes), "live:%d" % device, props,
                        int(props["warp_size"]))
     return mv if occupancy is None else _with_occupancy(mv, occupancy)
 

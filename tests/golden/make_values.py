@@ -1,0 +1,117 @@
+"""Generate tests/golden/value_vectors.json from the REFERENCE interpreter:
+values beyond the 32-bit words of interp_vectors.json.
+
+The reference interpreter stores Python objects (interp.py:76-81,
+183-206): binary64 floats at full precision, ints of any size, and -- for the
+programs that only move values -- whatever object the caller supplied.  This
+script runs parakern.interp.run_program (/root/reference/pkg/src/parakern/
+interp.py:215) on seeded instances of
+
+* reverse / transpose with binary64 floats (full 53-bit mantissas, -0.0,
+  subnormals, +-inf, 1e308), ints beyond int32 and int64, bools and mixed
+  int / float lists;
+* addition / matvec / matmul with binary64 floats (the executor's
+  PK_DTYPE_F64 path must reproduce them bit for bit) and with ints whose
+  results leave int32 (the int64 path) or int64 (recorded: the executor
+  raises OverflowError there);
+
+and records inputs and outputs.  Only this script touches /root/reference.
+
+    python tests/golden/make_values.py [--ref /root/reference/pkg/src]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+SPECIALS = [0.0, -0.0, 5e-324, -2.2250738585072014e-308, 1e308, -1.7976931348623157e308,
+            float("inf"), float("-inf"), 0.1, 1 / 3]
+
+
+def value(style: str, rng: random.Random):
+    if style == "f64":
+        r = rng.random()
+        if r < 0.15:
+            return rng.choice(SPECIALS)
+        return rng.uniform(-1.0, 1.0) * 10.0 ** rng.randrange(-30, 30)
+    if style == "f64_unit":
+        return rng.uniform(-1.0, 1.0)
+    if style == "i64":
+        return rng.randrange(-(2**62), 2**62)
+    if style == "bigint":
+        return rng.randrange(-(2**90), 2**90)
+    if style == "mixed":
+        return rng.choice([rng.randrange(-(2**40), 2**40), rng.uniform(-5, 5), True, False, 7])
+    if style == "i_wide":  # arithmetic: results leave int32, stay in int64
+        return rng.randrange(-(2**26), 2**26)
+    if style == "i_huge":  # arithmetic: results leave int64
+        return rng.randrange(-(2**40), 2**40)
+    raise KeyError(style)
+
+
+def fill(shape, style, rng):
+    if len(shape) == 1:
+        return [value(style, rng) for _ in range(shape[0])]
+    return [fill(shape[1:], style, rng) for _ in range(shape[0])]
+
+
+PARAMS = {
+    "reverse": [{"N": 64, "s": 2, "B": 8}, {"N": 37, "s": 2, "B": 8}, {"N": 16, "s": 1, "B": 4}],
+    "transpose": [{"N": 16, "s": 2, "B0": 4, "B1": 2}, {"N": 7, "s": 2, "B0": 3, "B1": 2}],
+    "addition": [{"N": 8, "B0": 2, "B1": 2}, {"N": 6, "B0": 4, "B1": 1}],
+    "matvec": [{"N": 16, "s": 2, "B": 4}, {"N": 11, "s": 2, "B": 3}],
+    "matmul": [{"n": 12, "B0": 4, "ub1": 2, "s": 2}, {"n": 10, "B0": 3, "ub1": 2, "s": 2}],
+}
+STYLES = {
+    "reverse": ["f64", "i64", "bigint", "mixed"],
+    "transpose": ["f64", "i64", "bigint", "mixed"],
+    "addition": ["f64", "f64_unit", "i_wide", "i_huge"],
+    "matvec": ["f64", "f64_unit", "i_wide", "i_huge"],
+    "matmul": ["f64_unit", "f64", "i_wide", "i_huge"],
+}
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg/src")
+    args = ap.parse_args()
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, args.ref)
+    from parakern import dsl, interp  # noqa: E402
+
+    from paper_1801_04348_b200 import programs  # noqa: E402
+
+    rng = random.Random(0x64F)
+    vectors = []
+    for family in sorted(PARAMS):
+        prog = dsl.parse(programs.original(family).text)
+        for params in PARAMS[family]:
+            for style in STYLES[family]:
+                shapes = {}
+                for name, data in interp.Machine(prog, dict(params)).arrays.items():
+                    shapes[name] = (len(data), len(data[0])) if data and isinstance(data[0], list) else (len(data),)
+                seed = {name: fill(shape, style, rng) for name, shape in shapes.items()}
+                if family in ("reverse", "transpose") and style != "mixed":
+                    seed.pop("c")  # the unwritten part of c stays int 0 (interp.py:79-81)
+                want = interp.run_program(prog, dict(params), arrays=seed)
+                vectors.append({"family": family, "params": params, "style": style, "inputs": seed,
+                                "outputs": want})
+    out = os.path.join(HERE, "value_vectors.json")
+    with open(out, "w") as fh:
+        json.dump({"generator": "parakern.interp.run_program via tests/golden/make_values.py",
+                   "seed": "0x64F", "vectors": vectors}, fh, separators=(",", ":"))
+        fh.write("\n")
+    print("wrote", out, len(vectors), "vectors", os.path.getsize(out), "bytes")
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -27,7 +27,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = _lib.load()
     for name in _declared_functions():
         assert hasattr(lib, name), name
-    assert _lib.version() == (1, 1)
+    assert _lib.version() == (1, 2)
     assert _lib.launch_count() >= 0
 
 
