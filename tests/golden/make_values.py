@@ -104,10 +104,33 @@ def main() -> int:
                 want = interp.run_program(prog, dict(params), arrays=seed)
                 vectors.append({"family": family, "params": params, "style": style, "inputs": seed,
                                 "outputs": want})
+    # IndexError (interp.py:209-212): the shortest 1-D array each program runs
+    # on without an out-of-bounds access -- what pk_required_elems must report
+    bounds = []
+    for family, params in [("reverse", {"N": 100, "s": 2, "B": 32}), ("reverse", {"N": 64, "s": 1, "B": 8}),
+                           ("matvec", {"N": 10, "s": 1, "B": 4}), ("matvec", {"N": 9, "s": 2, "B": 2}),
+                           ("jacobi", {"T": 1, "N": 10, "s": 2, "B": 2}),
+                           ("jacobi", {"T": 3, "N": 12, "s": 1, "B": 3})]:
+        prog = dsl.parse(programs.original(family).text)
+        full = interp.Machine(prog, dict(params)).arrays
+        mins = {}
+        for name, data in full.items():
+            if data and isinstance(data[0], list):
+                continue
+            n = len(data)
+            while n > 0:
+                arrays = {k: (list(v) if k != name else [0] * (n - 1)) for k, v in full.items()}
+                try:
+                    interp.run_program(prog, dict(params), arrays=arrays)
+                except IndexError:
+                    break
+                n -= 1
+            mins[name] = n
+        bounds.append({"family": family, "params": params, "min_len": mins})
     out = os.path.join(HERE, "value_vectors.json")
     with open(out, "w") as fh:
         json.dump({"generator": "parakern.interp.run_program via tests/golden/make_values.py",
-                   "seed": "0x64F", "vectors": vectors}, fh, separators=(",", ":"))
+                   "seed": "0x64F", "vectors": vectors, "bounds": bounds}, fh, separators=(",", ":"))
         fh.write("\n")
     print("wrote", out, len(vectors), "vectors", os.path.getsize(out), "bytes")
     return 0

@@ -73,3 +73,65 @@ def test_status_codes_map_to_reference_exceptions():
                     (_lib.PK_E_ALLOC, MemoryError), (_lib.PK_E_CUDA, _lib.PkError)]:
         with pytest.raises(exc):
             _lib.check(rc)
+
+
+def _launch(family, **kw):
+    L = _lib.PkLaunch()
+    L.family = _lib.FAMILY_IDS[family]
+    L.variant = _lib.VARIANT_STAGED
+    for k, v in kw.items():
+        setattr(L, k, v)
+    return L
+
+
+@pytest.mark.parametrize("family,kw,need", [
+    # reverse N=100, s*B=64: a[0..63] read, c[36..99] written
+    ("reverse", dict(N=100, s=2, B=32), [64, 100]),
+    ("reverse", dict(N=100, s=2, B=32, lo=8, hi=16), [16, 92]),
+    # transpose N=10, I = 9 rows (B0=3), J = 8 cols (s*B1=4): c[8*10+7], a[7][8]
+    ("transpose", dict(N=10, s=2, B0=3, B1=2), [7 * 10 + 9, 8 * 10 + 8]),
+    ("matvec", dict(N=10, s=1, B=4), [80, 10, 8]),
+    ("matmul", dict(N=10, B0=4, ub1=3, s=1), [7 * 10 + 8, 7 * 10 + 9, 7 * 10 + 9]),
+    ("addition", dict(N=8, B0=3, B1=2), [5 * 8 + 8, 5 * 8 + 8, 5 * 8 + 8]),
+    ("jacobi", dict(N=10, T=2, s=2, B=2), [20]),
+    ("jacobi", dict(N=10, T=0, s=2, B=2), [0]),
+    ("reverse", dict(N=100, s=-1, B=32), [0, 0]),
+])
+def test_required_elems_without_gpu(family, kw, need):
+    """pk_required_elems: 1 + the largest flat index the run touches (host-only)."""
+    assert _lib.required_elems(_launch(family, **kw), len(need)) == need
+
+
+def test_launch_checked_raises_index_error_before_launching():
+    """pk_launch_checked refuses short buffers with PK_E_BOUNDS (the
+    reference's IndexError, interp.py:209-212) before touching a device, so
+    it runs here without a GPU."""
+    L = _launch("reverse", N=100, s=2, B=32)
+    with pytest.raises(IndexError, match=r"c\[99\]"):
+        _lib.launch_checked(L, [0x1000, 0x2000], [100, 99])
+    with pytest.raises(IndexError, match=r"a\[63\]"):
+        _lib.launch_checked(L, [0x1000, 0x2000], [63, 100])
+    with pytest.raises(ZeroDivisionError):
+        _lib.launch_checked(_launch("reverse", N=100, s=0, B=32), [0x1000, 0x2000], [100, 100])
+    with pytest.raises(IndexError):
+        _lib.run_host(L, [0x1000, 0x2000], 0, elems=[100, 64])
+
+
+def test_required_elems_match_reference_index_errors():
+    """The shortest 1-D arrays the reference interpreter runs on without an
+    IndexError (tests/golden/make_values.py) == pk_required_elems."""
+    import json
+
+    with open(os.path.join(REPO, "tests", "golden", "value_vectors.json")) as fh:
+        bounds = json.load(fh)["bounds"]
+    from paper_1801_04348_b200 import binding, programs
+
+    for b in bounds:
+        if b["family"] == "jacobi":
+            continue  # the C ABI asks for the whole double buffer; the shim checks N+P+2 (GPU test)
+        kind = programs.original(b["family"])
+        L = binding.make_launch(kind, b["params"], ())
+        names = [a.name for a in programs.FAMILIES[b["family"]].arrays]
+        need = dict(zip(names, _lib.required_elems(L, len(names))))
+        for name, n in b["min_len"].items():
+            assert need[name] == n, (b, name)
