@@ -157,52 +157,98 @@ def timed_cpu(fn, budget_s: float, min_runs: int = 1):
             return el / runs, runs
 
 
-def cpu_matmul_sample(n: int, threads: int, budget_s: float):
-    """Oracle port (binary64, interpreter order) on an n x n sample."""
+# ------------------------------------------------------------- reference ----
+
+REF_ROWS = 64  # rows of the n = 8192 product per CPU step (8.6 GFLOP, ~0.1-0.2 s on 16 threads)
+
+
+def reference_interp_rate(fam: str):
+    """The reference interpreter's own rate (parakern.interp.run_program, one
+    core), measured in the build container by tools/time_reference_interp.py:
+    the reference cannot run on the GPU box."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r02_reference_interp.json")) as fh:
+            doc = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    rec = doc["families"].get(fam)
+    if rec is None:
+        return None
+    return {"value": rec["value"], "unit": rec["unit"], "cores": 1, "points_per_s": rec["points_per_s"],
+            "params": rec["params"], "where": doc["where"], "source": "profiles/r02_reference_interp.json"}
+
+
+def run_reference(args) -> int:
+    """The reference path on the host: the oracle port of interp.run_program
+    (binary64, all host threads) on the headline's own workload -- FP32
+    inputs of the n = 8192 matmul, each step a bounded block of REF_ROWS rows
+    of the product -- so value and unit compare with our arm directly."""
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return 0
     import numpy as np
 
     from oracle import oracle
 
+    n = args.n
+    threads = cpu_cores()
     oracle.build()
     oracle.set_threads(threads)
     rng = np.random.default_rng(0x1801)
     a = rng.uniform(-1, 1, (n, n)).astype(np.float32)
     b = rng.uniform(-1, 1, (n, n)).astype(np.float32)
-    P = {"n": n, "B0": 128 if n >= 128 else n, "ub1": 8 if n >= 128 else 1, "s": 16 if n >= 128 else 1}
-    sec, runs = timed_cpu(lambda: oracle.run("matmul", P, {"a": a, "b": b}), budget_s)
-    return 2.0 * n**3 / sec / 1e9, runs, sec
-
-
-# ------------------------------------------------------------- reference ----
-
-def run_reference(args) -> int:
-    rank, world, _ = dist_info()
-    if rank != 0:
-        return 0
-    n_sample = 1024
-    threads = cpu_cores()
-    vals = []
+    c = np.zeros((n, n))
+    P = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+    secs = []
     for i in range(args.warmup + args.steps):
-        gflops, runs, sec = cpu_matmul_sample(n_sample, threads, budget_s=0.0)
+        r0 = (i * REF_ROWS) % n
+        t0 = time.perf_counter()
+        oracle.matmul_rows_f64(P, r0, r0 + REF_ROWS, a, b, c)
         if i >= args.warmup:
-            vals.append((gflops, sec))
-    gf = statistics.median(v[0] for v in vals)
-    ms = statistics.median(v[1] for v in vals) * 1e3
-    sample = "matmul n=%d per step (2n^3 = %.3g FLOP), binary64 ascending-k, of the n=%d workload" % (
-        n_sample, 2.0 * n_sample**3, args.n)
+            secs.append(time.perf_counter() - t0)
+    sec = statistics.median(secs)
+    gf = 2.0 * REF_ROWS * n * n / sec / 1e9
+    sample = ("binary64 matmul of the n=%d workload (ascending k, unfused, the interpreter's order), "
+              "rows [r0, r0+%d) per step (%.3g FLOP)" % (n, REF_ROWS, 2.0 * REF_ROWS * n * n))
     line = {
         "metric": METRIC, "impl": "reference", "value": round(gf, 3), "unit": "GFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic U[-1,1) fp32 inputs, seed 0x1801",
-        "config": {"workload": "matmul n=%d fp32 (CPU sample n=%d)" % (args.n, n_sample),
-                   "parallelism": "host threads"},
+        "config": {"workload": "matmul n=%d fp32 FFMA, (B0,ub1,s) auto-tuned inside the live case" % n,
+                   "n": n, "parallelism": "host threads", "sample_rows_per_step": REF_ROWS},
         "cpu_baseline": {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(gf, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_interpreter": reference_interp_rate("matmul"),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def summary(line: dict) -> dict:
+    """Compact per-family record at the end of the line: value, fraction of
+    its roofline, the CPU port's rate on the box, and the parity verdict."""
+    def verdict(p):
+        if not p:
+            return None
+        return "ok" if (p == "exact" or p.startswith("within")) else "FAIL"
+
+    out = {"cols": ["value", "unit", "frac_roofline", "cpu_port", "parity"],
+           "matmul_n%d" % line["config"]["n"]: [line["value"], "GFLOP/s", line["roofline"]["frac"],
+                                                (line.get("cpu_baseline") or {}).get("value"),
+                                                verdict(line.get("parity"))]}
+    for fam, rec in (line.get("kernels") or {}).items():
+        if not isinstance(rec, dict) or "value" not in rec or "temporal" in fam:
+            continue
+        frac = rec.get("frac_of_measured_hbm", rec.get("frac_of_fp32_peak"))
+        out[fam] = [rec["value"], rec["unit"], frac, (rec.get("cpu_baseline") or {}).get("value"),
+                    verdict(rec.get("parity"))]
+    if line.get("e2e"):
+        out["e2e_c_abi"] = [line["e2e"]["value"], "GFLOP/s", None, None, None]
+    if line.get("e2e_run_program"):
+        out["e2e_run_program"] = [line["e2e_run_program"]["value"], "GFLOP/s", None, None, None]
+    return out
 
 
 # ------------------------------------------------------------------- ours ----
@@ -300,6 +346,15 @@ def main() -> int:
     flop_step = 2.0 * n * n * n  # whole job, all ranks
     value = flop_step / (ms_step * 1e-3) / 1e9
 
+    # parity of the measured leaf at full size, outside the timed region: one
+    # launch on fresh rows of c against a binary64 product of this rank's rows
+    # (N > 1: every rank checks its own share, the worst error is reported)
+    c.zero_()
+    err_t = torch.tensor([matmul_error(L, [a, b, c], n, r0, r0 + rows)], device=dev)
+    if world > 1:
+        dist.all_reduce(err_t, op=dist.ReduceOp.MAX)
+    headline_parity = parity_text(float(err_t.item()), n)
+
     # roofline of the dominant (only) kernel: FP32 FFMA pipe
     per_launch_flop = 2.0 * rows * n * n
     achieved_tf = per_launch_flop / (ms_local / args.steps * 1e-3) / 1e12
@@ -345,6 +400,31 @@ def main() -> int:
            "ms_per_step_min_max": [round(min(step_ms), 3), round(max(step_ms), 3)],
            "path": "pk_run_host (C ABI) with pinned host buffers, rank share of a/c and all of b"}
 
+    # the same call through the drop-in Python API with numpy host arrays
+    # (run_program stages them into pooled pinned buffers and calls pk_run_host)
+    e2e_api = None
+    if world == 1:
+        import numpy as np
+
+        from paper_1801_04348_b200 import run_program
+
+        na, nb = ha.numpy().reshape(n, n).copy(), hb.numpy().reshape(n, n).copy()
+        nc = np.zeros((n, n), dtype=np.float32)
+        text = programs.source("matmul")
+        for _ in range(2):
+            run_program(text, tuned, {"a": na, "b": nb, "c": nc})
+        api_ms = []
+        for _ in range(max(3, args.e2e_steps // 2)):
+            t1 = time.perf_counter()
+            out = run_program(text, tuned, {"a": na, "b": nb, "c": nc})
+            api_ms.append((time.perf_counter() - t1) * 1e3)
+        del out
+        e2e_api = {"value": round(flop_step / (statistics.mean(api_ms) * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": 3 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
+                   "ms_per_step_min_max": [round(min(api_ms), 3), round(max(api_ms), 3)],
+                   "path": "run_program(matmul.mfk, tuned, numpy float32 a/b/c): case selection, staging into "
+                           "pooled pinned buffers, pk_run_host, result copied into a fresh numpy array"}
+
     # optional 3xTF32 tcgen05 variant on the same shard (reported separately, never the headline)
     variants = {}
     try:
@@ -381,17 +461,15 @@ def main() -> int:
         kernels = bench_kernels_sharded(peaks, mv, rank, world)
     if rank == 0 and world == 1 and not args.no_kernels:
         del ha, hb, hc
-        kernels = bench_kernels(peaks, mv, args.no_tune)
+        kernels = bench_kernels(peaks, mv, args.no_tune, cpu=not args.no_cpu)
         try:
             kernels["emitted_baseline"] = bench_emitted(kernels)
         except Exception as exc:  # the baseline is informative only
             kernels["emitted_baseline"] = {"unavailable": str(exc)[:200]}
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = cpu_cores()
-        gf, runs, sec = cpu_matmul_sample(1024, threads, budget_s=10.0)
-        cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
-               "sample": "oracle/pk_oracle.c binary64 matmul n=1024 (2.15 GFLOP) x %d runs, %.3f s/run; "
-                         "the reference interpreter itself ran 46k FMA/s on 1 core (SURVEY 6)" % (runs, sec)}
+        # the same n = 8192 workload on the host: a row block of the product
+        cpu = cpu_matmul_rows(n, 0, REF_ROWS, cpu_cores())
+        cpu["reference_interpreter"] = reference_interp_rate("matmul")
 
     if rank == 0:
         line = {
@@ -412,12 +490,15 @@ def main() -> int:
                          "traffic": headline_traffic},
             "clocks": clocks,
             "e2e": e2e,
+            "e2e_run_program": e2e_api,
+            "parity": headline_parity,
             "gpu_launches": int(launches),
             "kernels": kernels,
             "variants": variants,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        line["summary"] = summary(line)  # last: the driver keeps the tail of stdout
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -425,25 +506,140 @@ def main() -> int:
     return 0
 
 
-def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
-    """The bandwidth-bound BASELINE configs on one GPU: GB/s of algorithmic
-    traffic and the fraction of the measured copy bandwidth."""
+def _fill(fam: str, shapes: dict, gen) -> list:
+    """Synthetic int32 inputs of a family in declaration order.  Ranges keep
+    every result inside int32 (mat-vec: |a|, |x| <= 2^7 at N = 32768), so the
+    C-int kernels and the reference's unbounded ints agree exactly."""
     import torch
 
-    from paper_1801_04348_b200 import _lib, binding, cases, programs
+    from paper_1801_04348_b200 import programs
 
-    from paper_1801_04348_b200 import autotune
+    lim = 1 << 7 if fam == "matvec" else 1 << 20
+    bufs = []
+    for arr in programs.FAMILIES[fam].arrays:
+        n = 1
+        for d in shapes[arr.name]:
+            n *= d
+        bufs.append(torch.randint(-lim, lim, (n,), dtype=torch.int32, device="cuda", generator=gen))
+    return bufs
+
+
+def restate(fam: str, P: dict, bufs: list) -> list:
+    """What the program leaves in its arrays, restated with torch on the GPU
+    from the initial contents (the checker of the bench's parity field; the
+    same restatements as tests/test_gpu_parity.py)."""
+    import torch
+
+    out = [b.clone() for b in bufs]
+    if fam == "reverse":
+        N, tile = P["N"], P["s"] * P["B"]
+        Pc = (N // tile) * tile
+        out[1][N - Pc:] = torch.flip(bufs[0][:Pc], [0])
+    elif fam == "transpose":
+        N, I, J = P["N"], (P["N"] // P["B0"]) * P["B0"], (P["N"] // (P["s"] * P["B1"])) * P["s"] * P["B1"]
+        out[1].view(N, N)[:I, :J] = bufs[0].view(N, N).t()[:I, :J]
+    elif fam == "jacobi":
+        N, tile = P["N"], P["s"] * P["B"]
+        Pc = ((N - 2) // tile) * tile
+        h = [out[0][:N], out[0][N:]]
+        for t in range(P["T"]):
+            src, dst = (h[1], h[0]) if t % 2 == 0 else (h[0], h[1])
+            s = src[0:Pc].long() + src[1:Pc + 1] + src[2:Pc + 2]
+            dst[1:Pc + 1] = torch.div(s, 3, rounding_mode="trunc").int()
+    elif fam == "jacobi2d":
+        N = P["N"]
+        I, J = ((N - 2) // P["B0"]) * P["B0"], ((N - 2) // (P["s"] * P["B1"])) * P["s"] * P["B1"]
+        a = out[0].view(2 * N, N)
+        h = [a[:N], a[N:]]
+        for t in range(P["T"]):
+            src, dst = (h[0], h[1]) if t % 2 == 0 else (h[1], h[0])
+            s = (src[0:I, 1:J + 1].long() + src[2:I + 2, 1:J + 1] + src[1:I + 1, 0:J] + src[1:I + 1, 2:J + 2]
+                 + src[1:I + 1, 1:J + 1])
+            dst[1:I + 1, 1:J + 1] = torch.div(s, 5, rounding_mode="trunc").int()
+    elif fam == "matvec":
+        N, tile = P["N"], P["s"] * P["B"]
+        R = (N // tile) * tile
+        a = bufs[0].view(N, N)[:R].double()
+        out[2][:R] = (bufs[2][:R].double() + a @ bufs[1].double()).round().int()  # |sums| < 2^53: exact
+    elif fam == "addition":
+        N = P["N"]
+        I = (N // P["B0"]) * P["B0"]
+        J, half = min((N // (2 * P["B1"])) * P["B1"], N // 2), N // 2
+        a, b, c = (x.view(N, N) for x in (bufs[0], bufs[1], out[2]))
+        c[:I, :J] = a[:I, :J] + b[:I, :J]
+        c[:I, half:half + J] = a[:I, half:half + J] + b[:I, half:half + J]
+    else:
+        raise KeyError(fam)
+    return out
+
+
+def parity_check(fam: str, P: dict, L, gen) -> str:
+    """One run of the measured leaf on fresh inputs, outside the timed
+    region, against restate(): "exact" or the first mismatch."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, programs
+
+    bufs = _fill(fam, programs.array_shapes(programs.original(fam), P), gen)
+    want = restate(fam, P, bufs)
+    _lib.launch(L, [b.data_ptr() for b in bufs], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for i, (g, w) in enumerate(zip(bufs, want)):
+        if not torch.equal(g, w):
+            bad = int((g != w).nonzero()[0, 0])
+            return "MISMATCH array %d at %d" % (i, bad)
+    return "exact"
+
+
+# bounded CPU samples of each family for the oracle port (all host threads)
+CPU_SAMPLES = {
+    "reverse": ({"N": 1 << 27, "s": 16, "B": 256}, lambda P: 8 * P["N"], "GB/s"),
+    "transpose": ({"N": 8192, "s": 8, "B0": 64, "B1": 8}, lambda P: 8 * P["N"] ** 2, "GB/s"),
+    "jacobi": ({"T": 4, "N": (1 << 26) + 2, "s": 16, "B": 256}, lambda P: P["T"] * 8 * (P["N"] - 2), "GB/s"),
+    "jacobi2d": ({"T": 4, "N": 4098, "s": 4, "B0": 8, "B1": 32}, lambda P: P["T"] * 8 * (P["N"] - 2) ** 2, "GB/s"),
+    "matvec": ({"N": 16384, "s": 1, "B": 512}, lambda P: 4 * P["N"] ** 2 + 8 * P["N"], "GB/s"),
+    "addition": ({"N": 8192, "B0": 8, "B1": 128}, lambda P: 12 * P["N"] ** 2, "GB/s"),
+}
+
+
+def cpu_sample(fam: str, threads: int) -> dict:
+    """The reference path's CPU restatement (oracle/pk_oracle.c, OpenMP over
+    all host threads) on a bounded sample of the family's workload."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1801_04348_b200 import programs
+
+    oracle.build()
+    oracle.set_threads(threads)
+    P, work, unit = CPU_SAMPLES[fam]
+    shapes = programs.array_shapes(programs.original(fam), P)
+    rng = np.random.default_rng(0x1801)
+    lim = 1 << 7 if fam == "matvec" else 1 << 20
+    arrays = {k: rng.integers(-lim, lim, size=v, dtype=np.int32) for k, v in shapes.items()}
+    oracle.run(fam, dict(P, T=1) if "T" in P else P, arrays)  # page in, warm the threads
+    sec, runs = timed_cpu(lambda: oracle.run(fam, P, arrays), budget_s=1.0)
+    return {"value": round(work(P) / sec / 1e9, 3), "unit": unit, "cores": threads, "kind": "port",
+            "sample": "oracle/pk_oracle.c on %s, %.3f s/run x %d" % (json.dumps(P), sec, runs)}
+
+
+def bench_kernels(peaks, mv, no_tune: bool = False, cpu: bool = True) -> dict:
+    """The bandwidth-bound BASELINE configs on one GPU: GB/s of algorithmic
+    traffic and the fraction of the measured copy bandwidth, each with a
+    parity check of the measured leaf at full size and the oracle port's
+    rate on a bounded CPU sample."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, autotune, binding, cases, programs
 
     out = {}
+    threads = cpu_cores()
+    gen = torch.Generator(device="cuda")
     for fam, (params, work, unit) in KERNEL_CONFIGS.items():
         kind = programs.original(fam)
         shapes = programs.array_shapes(kind, params)
-        bufs = []
-        for arr in programs.FAMILIES[fam].arrays:
-            n = 1
-            for d in shapes[arr.name]:
-                n *= d
-            bufs.append(torch.randint(-(1 << 20), 1 << 20, (n,), dtype=torch.int32, device="cuda"))
+        gen.manual_seed(0x1801)
+        bufs = _fill(fam, shapes, gen)
         ptrs = [x.data_ptr() for x in bufs]
         # tune (B, s) / (B0, B1, s) inside the live case on 2 time steps, run the full T
         tune_base = dict(params, T=2) if "T" in params else dict(params)
@@ -497,6 +693,13 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
                             "because h steps share one HBM pass; results bit-identical"}
         del bufs
         torch.cuda.empty_cache()
+        out[fam]["parity"] = parity_check(fam, run_params, L, gen)
+        torch.cuda.empty_cache()
+        if cpu:
+            try:
+                out[fam]["cpu_baseline"] = cpu_sample(fam, threads)
+            except Exception as exc:  # informative only
+                out[fam]["cpu_baseline"] = {"unavailable": str(exc)[:200]}
     # mat-vec on float32 data (SURVEY 8(d) proposes N = 32768 FP32): double-float accumulation
     if "matvec" in out and "params" in out["matvec"]:
         mp = dict(out["matvec"]["params"])
@@ -520,13 +723,66 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
         gbs = (4 * Nm * Nm + 8 * Nm) / (ms * 1e-3) / 1e9
+        # parity: one launch from y = 0 against a binary64 product, 2 fp32 ulps
+        bufs[2].zero_()
+        _lib.launch(L, ptrs, st.cuda_stream)
+        want = bufs[0].view(Nm, Nm).double() @ bufs[1].double()
+        ok = bool(((bufs[2].double() - want).abs() <= 2 * 2.0**-24 * want.abs() + 1e-30).all())
         out["matvec_f32"] = {"params": mp, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3),
                              "value": round(gbs, 1), "unit": "GB/s",
                              "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
+                             "parity": "within 2 fp32 ulps of binary64" if ok else "MISMATCH",
                              "note": "float32 a, x, y; products split exactly and summed as a double-float pair"}
-        del bufs
+        del bufs, want
         torch.cuda.empty_cache()
-    # the other size of BASELINE configs[1]: FP32 matmul n = 2048, (B0, ub1, s) tuned inside the case
+    out["addition"] = bench_addition(peaks, mv, threads if cpu else 0)
+    out["matmul_n2048"] = bench_matmul_n2048(peaks, mv, no_tune, threads if cpu else 0)
+    return out
+
+
+def bench_addition(peaks, mv, threads: int) -> dict:
+    """addition.mfk, N = 16384: 12 bytes per element."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, binding, cases, programs
+
+    P = {"N": 16384, "B0": 8, "B1": 128}
+    kind = programs.original("addition")
+    sel = cases.select(kind, P, mv)
+    L = binding.make_launch(kind, P, sel.applied, _lib.DTYPE_I32)
+    gen = torch.Generator(device="cuda").manual_seed(0x1801)
+    bufs = _fill("addition", programs.array_shapes(kind, P), gen)
+    ptrs = [x.data_ptr() for x in bufs]
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(10):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    work = 12 * P["N"] ** 2
+    gbs = work / (ms * 1e-3) / 1e9
+    del bufs
+    torch.cuda.empty_cache()
+    rec = {"params": P, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3), "value": round(gbs, 1),
+           "unit": "GB/s", "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
+           "parity": parity_check("addition", P, L, gen)}
+    if threads:
+        rec["cpu_baseline"] = cpu_sample("addition", threads)
+    return rec
+
+
+def bench_matmul_n2048(peaks, mv, no_tune: bool, threads: int) -> dict:
+    """The other size of BASELINE configs[1]: FP32 matmul n = 2048, (B0, ub1, s)
+    tuned inside the case."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, autotune, binding, cases, programs
+
     n2 = 2048
     kind = programs.original("matmul")
     base = {"n": n2, "B0": 128, "ub1": 8, "s": 16}
@@ -553,13 +809,61 @@ def bench_kernels(peaks, mv, no_tune: bool = False) -> dict:
     ms = e0.elapsed_time(e1) / 20
     gf = 2.0 * n2 ** 3 / (ms * 1e-3) / 1e9
     peak = mv.props.get("sm_count", 148) * 256 * peaks["sm_max_mhz"] * 1e6 / 1e9
-    out["matmul_n2048"] = {"params": tuned, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 4),
-                           "value": round(gf, 1), "unit": "GFLOP/s", "frac_of_fp32_peak": round(gf / peak, 4),
-                           "tuning_trials": len(trials),
-                           "note": "256 tiles of 128 x 128 on 296 resident CTA slots: 0.86 of one wave"}
+    bufs[2].zero_()
+    err = matmul_error(L, bufs, n2, 0, n2)
+    rec = {"params": tuned, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 4),
+           "value": round(gf, 1), "unit": "GFLOP/s", "frac_of_fp32_peak": round(gf / peak, 4),
+           "tuning_trials": len(trials), "parity": parity_text(err, n2)}
     del bufs
     torch.cuda.empty_cache()
-    return out
+    if threads:
+        rec["cpu_baseline"] = cpu_matmul_rows(n2, 0, n2, threads)
+    return rec
+
+
+def matmul_error(L, bufs, n: int, r0: int, r1: int) -> float:
+    """One launch of L on (a, b, c) and the normalised error of rows [r0, r1)
+    of c against a binary64 product: max|C - C64| / max sum_k |a_ik b_kj|."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib
+
+    a, b, c = (x.view(n, n) for x in bufs)
+    c0 = c[r0:r1].double()
+    _lib.launch(L, [x.data_ptr() for x in bufs], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    a64, b64 = a[r0:r1].double(), b.double()
+    want = c0 + a64 @ b64
+    scale = (a64.abs() @ b64.abs()).max()
+    return float(((c[r0:r1].double() - want).abs().max() / scale).item())
+
+
+def parity_text(err: float, K: int) -> str:
+    tol = max(1e-5 * K / 1024.0, 2.0 * K * 2.0**-24)
+    return "%s: normalised error %.3g vs tolerance %.3g (1e-5*K/1024)" % ("within" if err <= tol else "MISMATCH",
+                                                                         err, tol)
+
+
+def cpu_matmul_rows(n: int, r0: int, r1: int, threads: int) -> dict:
+    """Rows [r0, r1) of the n x n matmul in binary64 by the oracle port (all
+    host threads): a bounded sample of the same workload, GFLOP/s."""
+    import numpy as np
+
+    from oracle import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    rng = np.random.default_rng(0x1801)
+    a = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    b = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    c = np.zeros((n, n))
+    P = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+    oracle.matmul_rows_f64(P, r0, min(r1, r0 + 8), a, b, c)  # warm the threads
+    sec, runs = timed_cpu(lambda: oracle.matmul_rows_f64(P, r0, r1, a, b, c), budget_s=1.0)
+    flop = 2.0 * (r1 - r0) * n * n
+    return {"value": round(flop / sec / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": "oracle/pk_oracle.c binary64 matmul n=%d, rows [%d, %d) of the product (%.3g FLOP), "
+                      "%.3f s/run x %d" % (n, r0, r1, flop, sec, runs)}
 
 
 def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:

@@ -56,6 +56,7 @@ def lib():
             "pko_matvec_f64": [i64, i64, i64, P, P, P],
             "pko_matmul_i32": [i64, i64, i64, i64, P, P, P],
             "pko_matmul_f64": [i64, i64, i64, i64, P, P, P],
+            "pko_matmul_f64_rows": [i64, i64, i64, i64, i64, i64, P, P, P],
             "pko_addition_i32": [i64, i64, i64, P, P, P],
         }
         for name, args in sig.items():
@@ -94,6 +95,14 @@ def _i32(x, shape):
 
 def _is_float(x) -> bool:
     return x is not None and np.issubdtype(np.asarray(x).dtype, np.floating)
+
+
+def matmul_rows_f64(params: dict, r0: int, r1: int, a: np.ndarray, b: np.ndarray, c: np.ndarray) -> None:
+    """Rows [r0, r1) of the matmul program in binary64 (in place on c, float64
+    n x n; a, b float32 n x n) -- a bounded sample of one full run."""
+    P = {k: int(v) for k, v in params.items()}
+    assert a.dtype == np.float32 and b.dtype == np.float32 and c.dtype == np.float64
+    _check(lib().pko_matmul_f64_rows(P["n"], P["B0"], P["ub1"], P["s"], r0, r1, _p(a), _p(b), _p(c)), "matmul")
 
 
 def run(family: str, params: dict, arrays: dict | None = None, *, merged: bool = False) -> dict:

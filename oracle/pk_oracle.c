@@ -192,6 +192,9 @@ int pko_matvec_f64(i64 N, i64 s, i64 B, const float *a, const float *x, double *
  *   p < dim0*B0, q < dim1*ub1*s; the reduction index kk = B0*k+z runs
  *   ascending over [0, kdim*B0) for every output.
  * ------------------------------------------------------------------------- */
+int pko_matmul_f64_rows(i64 n, i64 B0, i64 ub1, i64 s, i64 r0, i64 r1, const float *a, const float *b,
+                        double *c);
+
 static void matmul_extents(i64 n, i64 B0, i64 ub1, i64 s, i64 *M, i64 *Nc, i64 *K) {
     i64 dim0 = c_div(n, B0), dim1 = c_div(n, ub1 * s), kdim = c_div(n, B0);
     *M = max0(dim0) * B0;
@@ -216,11 +219,19 @@ int pko_matmul_i32(i64 n, i64 B0, i64 ub1, i64 s, const int32_t *a, const int32_
 }
 
 int pko_matmul_f64(i64 n, i64 B0, i64 ub1, i64 s, const float *a, const float *b, double *c) {
+    return pko_matmul_f64_rows(n, B0, ub1, s, 0, n, a, b, c);
+}
+
+/* The rows [r0, r1) of the same program (a bounded sample of one run: the
+ * rows are independent, every output keeps its ascending-kk sequence). */
+int pko_matmul_f64_rows(i64 n, i64 B0, i64 ub1, i64 s, i64 r0, i64 r1, const float *a, const float *b, double *c) {
     if (B0 == 0 || ub1 * s == 0) return PKO_E_DIV0;
     i64 M, Nc, K;
     matmul_extents(n, B0, ub1, s, &M, &Nc, &K);
+    if (r0 < 0) r0 = 0;
+    if (r1 > M) r1 = M;
     #pragma omp parallel for schedule(static)
-    for (i64 p = 0; p < M; p++) {
+    for (i64 p = r0; p < r1; p++) {
         double *crow = c + p * n;
         /* ascending kk per output; the q loop is innermost only for cache
          * locality -- every c[p][q] still sees kk = 0, 1, 2, ... in order */

@@ -244,7 +244,7 @@ def run_program(
         leaf = jit.emit_leaf(program, params)
         _last = RunInfo("emitted", None, tuple(leaf.applied), False, {"kernel": leaf.kernel_name}, 0)
         return jit.run_program_jit(leaf, params, arrays)
-    rename = getattr(kind, "rename", None) or {}
+    rename = dict(kind.rename)
     if rename:  # an alpha-renamed copy of a known program: speak the family's names inside
         params = {rename.get(k, k): v for k, v in params.items()}
         arrays = {rename.get(k, k): v for k, v in (arrays or {}).items()}

@@ -43,6 +43,23 @@ def normalize(text: str) -> str:
     return " ".join(out)
 
 
+# the DSL's keywords (dsl.py:48); every other identifier may be renamed
+KEYWORDS = frozenset({"int", "for", "if", "else", "meta_schedule", "meta_for", "cache"})
+
+
+def alpha(key: str) -> tuple[str, list[str]]:
+    """A normalised token stream with identifiers renamed by first
+    appearance (x0, x1, ...), and the original identifiers in that order:
+    two programs that differ only by a consistent renaming share the key."""
+    names: dict[str, str] = {}
+    out = []
+    for tok in key.split(" "):
+        if (tok[0].isalpha() or tok[0] == "_") and tok not in KEYWORDS:
+            tok = names.setdefault(tok, "x%d" % len(names))
+        out.append(tok)
+    return " ".join(out), list(names)
+
+
 def _c_div(a: int, b: int) -> int:
     """C99 truncating division (interp.py:43-46)."""
     q = abs(a) // abs(b)
@@ -125,6 +142,7 @@ class ProgramKind:
     applied: tuple[str, ...]  # subset of SOURCE_STRATEGIES, in application order
     params: tuple[str, ...]  # scalar parameters this text declares
     text: str = field(compare=False, repr=False, default="")
+    rename: tuple = field(compare=False, repr=False, default=())  # (caller's name, family's name) pairs
 
     @property
     def is_original(self) -> bool:
@@ -174,12 +192,34 @@ def program_text(program) -> str:
     raise TypeError("program must be .mfk text, a path to a .mfk file or a parakern Program")
 
 
+@lru_cache(maxsize=1)
+def alpha_registry() -> dict[str, tuple[ProgramKind, list[str]]]:
+    """Alpha-normalised text -> (ProgramKind, its identifiers in first-appearance order)."""
+    out = {}
+    for key, kind in registry().items():
+        akey, names = alpha(key)
+        out.setdefault(akey, (kind, names))
+    return out
+
+
 def identify(program) -> ProgramKind:
-    """Recognise a program; NotImplementedError for shapes without a kernel."""
+    """Recognise a program; NotImplementedError for shapes without a kernel.
+
+    A program that differs from a known one only by a consistent renaming of
+    its identifiers (parameters, arrays, bindings, loop variables) is that
+    program: the returned kind carries ``rename`` pairs (caller's name ->
+    family's name) that run_program applies to params and arrays."""
     if isinstance(program, ProgramKind):
         return program
     key = normalize(program_text(program))
     kind = registry().get(key)
+    if kind is None:
+        akey, names = alpha(key)
+        hit = alpha_registry().get(akey)
+        if hit is not None:
+            known, known_names = hit
+            pairs = tuple((u, k) for u, k in zip(names, known_names) if u != k)
+            return ProgramKind(known.family, known.applied, known.params, known.text, pairs)
     if kind is None:
         raise NotImplementedError(
             "no sm_100a kernel family matches this program; the executor binds "

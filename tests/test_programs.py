@@ -63,3 +63,26 @@ def test_binding_variants():
     assert L.flags & _lib.FLAG_MERGED
     L = binding.make_launch(programs.original("addition"), {"N": 8, "B0": 2, "B1": 2}, ("granularity",))
     assert not (L.flags & _lib.FLAG_MERGED)
+
+
+def test_alpha_renamed_programs_are_recognised():
+    """A consistent renaming of identifiers is the same program (the caller's
+    names map onto the family's); an inconsistent one is not."""
+    import re
+
+    import pytest
+
+    from paper_1801_04348_b200 import programs
+
+    for family in programs.FAMILIES:
+        text = programs.source(family)
+        names = programs.alpha(programs.normalize(text))[1]
+        renamed = text
+        for i, n in enumerate(names):
+            renamed = re.sub(r"\b%s\b" % n, "zz%d_%s" % (i, n), renamed)
+        kind = programs.identify(renamed)
+        assert kind.family == family and kind.is_original
+        assert dict(kind.rename) == {"zz%d_%s" % (i, n): n for i, n in enumerate(names)}
+    broken = programs.source("reverse").replace("c[N - 1 - p]", "a[N - 1 - p]")  # writes a, not c
+    with pytest.raises(NotImplementedError):
+        programs.identify(broken)
