@@ -48,19 +48,42 @@ __device__ __forceinline__ bool r_narrow(int mode, const int *flag) {
     return v != 0;
 }
 
-__device__ __forceinline__ int4 ldq(const int *p) { return __ldg(reinterpret_cast<const int4 *>(p)); }
+// Loads of the source half.  COH = false: the read-only (.nc) path -- the
+// half was written by earlier kernels only.  COH = true: the edge blocks of
+// a peer sweep, whose ghost rows a neighbouring GPU stores over NVLink while
+// this kernel runs; they load through the coherent path (weak ld.global.cg,
+// L2 -- the point of coherence for this GPU's memory), ordered after thread
+// 0's ld.acquire.sys of the neighbour's counter by the block barrier, which
+// the non-coherent .nc path is not.
+template <bool COH = false>
+__device__ __forceinline__ int4 ldq(const int *p) {
+    if (!COH) return __ldg(reinterpret_cast<const int4 *>(p));
+    int4 r;
+    asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p)
+                 : "memory");
+    return r;
+}
+template <bool COH = false>
+__device__ __forceinline__ int ld1(const int *p) {
+    if (!COH) return __ldg(p);
+    int r;
+    asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
 
 // 16-byte quad at element y of a length-n array (y % 4 on a 16-byte boundary);
 // elements outside [0, n) read as 0 (they only feed outputs never stored)
+template <bool COH = false>
 __device__ __forceinline__ int4 ldq_guard(const int *a, int64_t y, int64_t n) {
-    if (y >= 0 && y + 3 < n) return ldq(a + y);
+    if (y >= 0 && y + 3 < n) return ldq<COH>(a + y);
     int t[4];
 #pragma unroll
-    for (int e = 0; e < 4; e++) t[e] = (y + e >= 0 && y + e < n) ? __ldg(a + y + e) : 0;
+    for (int e = 0; e < 4; e++) t[e] = (y + e >= 0 && y + e < n) ? ld1<COH>(a + y + e) : 0;
     return make_int4(t[0], t[1], t[2], t[3]);
 }
+template <bool COH = false>
 __device__ __forceinline__ int ld1_guard(const int *a, int64_t y, int64_t n) {
-    return (y >= 0 && y < n) ? __ldg(a + y) : 0;
+    return (y >= 0 && y < n) ? ld1<COH>(a + y) : 0;
 }
 __device__ __forceinline__ int q_at(const int4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
@@ -168,6 +191,25 @@ __device__ __forceinline__ void j1r_compute(const int4 (&own)[K], const int4 (&e
     }
 }
 
+template <int D, int K, bool COH>
+__device__ __forceinline__ void j1r_load(const int *__restrict__ s, int64_t xw, int64_t N, bool interior,
+                                         int4 (&own)[K], int4 (&edge)[K]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const int64_t y = xw + 4 * (lane + 32 * j) + D;
+        own[j] = interior ? ldq<COH>(s + y) : ldq_guard<COH>(s, y, N);
+    }
+    // the quads across the warp edges, loaded once the warp's own loads are in
+    // flight (the neighbouring warp's loads of the same sectors are then L1 hits)
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const int64_t y = xw + 4 * (lane + 32 * j) + D;
+        if (lane == 0) edge[j] = interior ? ldq<COH>(s + y - 4) : ldq_guard<COH>(s, y - 4, N);
+        if (D == 0 && lane == 31) edge[j].x = interior ? ld1<COH>(s + y + 4) : ld1_guard<COH>(s, y + 4, N);
+    }
+}
+
 // The loads do not depend on the sum width: they are issued first, the
 // narrow flag (a device word set by the range pre-pass) is read beside
 // them, and only the arithmetic branches on it.
@@ -190,19 +232,10 @@ __global__ void __launch_bounds__(kJ1Threads) k_jacobi1d_reg(const int *__restri
     // warp-uniform: every load inside [0, N) and every store inside [lo, hi)
     const bool interior = xw + D - 4 >= 0 && xw + 4 * 32 * K + D + 4 <= N && xw >= lo && xw + 4 * 32 * K <= hi;
     int4 own[K], edge[K];
-#pragma unroll
-    for (int j = 0; j < K; j++) {
-        const int64_t y = xw + 4 * (lane + 32 * j) + D;
-        own[j] = interior ? ldq(s + y) : ldq_guard(s, y, N);
-    }
-    // the quads across the warp edges, loaded once the warp's own loads are in
-    // flight (the neighbouring warp's loads of the same sectors are then L1 hits)
-#pragma unroll
-    for (int j = 0; j < K; j++) {
-        const int64_t y = xw + 4 * (lane + 32 * j) + D;
-        if (lane == 0) edge[j] = interior ? ldq(s + y - 4) : ldq_guard(s, y - 4, N);
-        if (D == 0 && lane == 31) edge[j].x = interior ? __ldg(s + y + 4) : ld1_guard(s, y + 4, N);
-    }
+    if (PEER && (pl || pr))
+        j1r_load<D, K, true>(s, xw, N, interior, own, edge);
+    else
+        j1r_load<D, K, false>(s, xw, N, interior, own, edge);
     if (narrow)
         j1r_compute<false, D, K, PEER>(own, edge, d, xw, lo, hi, interior, &P);
     else
@@ -271,7 +304,7 @@ __device__ __forceinline__ void j2r_compute(const RowQ (&rows)[kJ2R + 2], int *_
     }
 }
 
-template <bool PH2, bool EDGE, bool PEER = false>
+template <bool PH2, bool EDGE, bool PEER = false, bool COH = false>
 __device__ __forceinline__ void j2r_band(const int *__restrict__ s, int *__restrict__ d, int64_t N, int64_t i0,
                                          int64_t c, int64_t lo, int64_t hi, int64_t J, bool narrow,
                                          const PeerSweep *P = nullptr) {
@@ -284,9 +317,9 @@ __device__ __forceinline__ void j2r_band(const int *__restrict__ s, int *__restr
     for (int u = 0; u < R + 2; u++) {
         const int sh = (PH2 && (u & 1)) ? 2 : 0;
         if (!EDGE)
-            raw[u] = ldq(rp + sh);
+            raw[u] = ldq<COH>(rp + sh);
         else if (u < nl)
-            raw[u] = ldq_guard(rp - c, c + sh, N);
+            raw[u] = ldq_guard<COH>(rp - c, c + sh, N);
         rp += N;
     }
     // the quads across the warp edges after the warp's own loads (L1 hits then)
@@ -296,11 +329,11 @@ __device__ __forceinline__ void j2r_band(const int *__restrict__ s, int *__restr
         const bool ph = PH2 && (u & 1);
         const int sh = ph ? 2 : 0;
         if (!EDGE) {
-            if (lane == 0) ext[u] = ldq(rp - 4 + sh);
-            if (lane == 31 && !ph) ext[u].x = __ldg(rp + 4);
+            if (lane == 0) ext[u] = ldq<COH>(rp - 4 + sh);
+            if (lane == 31 && !ph) ext[u].x = ld1<COH>(rp + 4);
         } else if (u < nl) {
-            if (lane == 0) ext[u] = ldq_guard(rp - c, c - 4 + sh, N);
-            if (lane == 31 && !ph) ext[u].x = ld1_guard(rp - c, c + 4, N);
+            if (lane == 0) ext[u] = ldq_guard<COH>(rp - c, c - 4 + sh, N);
+            if (lane == 31 && !ph) ext[u].x = ld1_guard<COH>(rp - c, c + 4, N);
         }
         rp += N;
     }
@@ -352,10 +385,16 @@ __global__ void __launch_bounds__(kJ2Warps * 32) k_jacobi2d_reg(const int *__res
     const int64_t i0 = rs + rb * kJ2R;  // odd: loaded row u has the phase of u
     const bool interior = cblk >= 4 && cblk + kJ2Warps * 128 + 8 <= N && cblk + kJ2Warps * 128 <= J + 1 &&
                           i0 >= lo && i0 + kJ2R <= hi;
-    if (interior)
+    if (PEER && (pl || pr)) {  // the bands reading a ghost row a neighbour stores: coherent loads
+        if (interior)
+            j2r_band<PH2, false, PEER, true>(s, d, N, i0, c, lo, hi, J, narrow, &P);
+        else
+            j2r_band<PH2, true, PEER, true>(s, d, N, i0, c, lo, hi, J, narrow, &P);
+    } else if (interior) {
         j2r_band<PH2, false, PEER>(s, d, N, i0, c, lo, hi, J, narrow, &P);
-    else
+    } else {
         j2r_band<PH2, true, PEER>(s, d, N, i0, c, lo, hi, J, narrow, &P);
+    }
     if (PEER && (pl || pr)) peer_signal(P, pl, pr);
 }
 

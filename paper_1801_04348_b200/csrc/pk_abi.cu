@@ -880,7 +880,11 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         unsigned *ctr[kMaxDevices] = {};
         for (int k = 0; k < ndev && rc == PK_OK; k++) {  // [from_left, from_right, error] per device
             cudaSetDevice(devices[k]);
-            cudaError_t e = cudaMallocAsync((void **)&ctr[k], 4 * sizeof(unsigned), M.st[k]);
+            // cudaMalloc, not the stream-ordered pool: the neighbours' kernels
+            // bump these counters with system-scope atomics over NVLink, and
+            // peer access (cudaDeviceEnablePeerAccess) covers cudaMalloc
+            // memory but not a memory pool without cudaMemPoolSetAccess
+            cudaError_t e = cudaMalloc((void **)&ctr[k], 4 * sizeof(unsigned));
             if (e == cudaSuccess) e = cudaMemsetAsync(ctr[k], 0, 4 * sizeof(unsigned), M.st[k]);
             if (e == cudaSuccess) e = cudaEventRecord(M.done[k], M.st[k]);
             if (e != cudaSuccess) rc = fail(PK_E_CUDA, "peer counters on device %d: %s", devices[k], cudaGetErrorString(e));
@@ -916,7 +920,12 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
         for (int k = 0; k < ndev; k++) {  // every device done before any counter goes away
             if (!ctr[k]) continue;
             cudaSetDevice(devices[k]);
-            cudaFreeAsync(ctr[k], M.st[k]);
+            cudaStreamSynchronize(M.st[k]);
+        }
+        for (int k = 0; k < ndev; k++) {
+            if (!ctr[k]) continue;
+            cudaSetDevice(devices[k]);
+            cudaFree(ctr[k]);
         }
         if (rc == PK_OK && err) rc = fail(PK_E_CUDA, "pk_launch_multi: a peer wait timed out");
     }

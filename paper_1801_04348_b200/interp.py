@@ -24,6 +24,7 @@ on the caller's device buffers without copies.
 
 from __future__ import annotations
 
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -307,20 +308,45 @@ def run_program(
     runnable = all(counts[n] > 0 for n in declared)
     on_device = any(s.kind == "torch" and s.value.is_cuda for s in srcs.values())
     multi = devices is not None and len(devices) > 1
-    words = {}
+    words, out, owned = {}, {}, False
+    written = set(fam.written)
     if not on_device and not multi and not inplace:
-        # host arrays: pinned staging + pk_run_host (copies overlap the kernels)
+        # host arrays: pinned staging + pk_run_host (its PCIe copies overlap the
+        # kernels); while the GPU runs, this thread copies out the arrays the
+        # program never writes (the reference deep-copies them, interp.py:183-186)
+        owned = True
         with _pinned.lock:
             bufs = []
             for i, n in enumerate(declared):
                 buf = _pinned.view(i, counts[n], plan.np_dtype)
                 marshal.host_words(plan, srcs.get(n), counts[n], buf)
                 bufs.append(buf)
+            failure = []
+            worker = None
             if runnable:
-                with torch.cuda.device(dev):
-                    _lib.run_host(L, [b.ctypes.data for b in bufs], dev.index, elems=[counts[n] for n in declared])
+                def work():
+                    try:
+                        _lib.run_host(L, [b.ctypes.data for b in bufs], dev.index,
+                                      elems=[counts[n] for n in declared])
+                    except BaseException as exc:  # re-raised on the caller's thread
+                        failure.append(exc)
+
+                worker = threading.Thread(target=work, name="pk_run_host")
+                worker.start()
+            try:
+                for n in declared:
+                    if n not in written:
+                        like = arrays.get(n)
+                        k = marshal.kind_of(like) if like is not None else default_kind
+                        out[n] = marshal.copy_input(plan, srcs.get(n), shapes[n], k, like)
+            finally:
+                if worker is not None:
+                    worker.join()
+            if failure:
+                raise failure[0]
             for n, buf in zip(declared, bufs):
-                words[n] = buf[: counts[n]].copy()
+                if n in written:
+                    words[n] = marshal.fresh_copy(buf[: counts[n]])
     else:
         stream = torch.cuda.current_stream(dev).cuda_stream
         with torch.cuda.device(dev):
@@ -353,19 +379,20 @@ def run_program(
     _last = RunInfo(kind.family, case_index, tuple(applied), fallback, binding.describe(L),
                     _lib.footprint_words(L))
 
-    out = {}
     # arrays the caller passed that the program does not declare come back as copies
     for name, v in arrays.items():
         if name not in counts:
             out[name] = _deep_copy(v)
     for n in declared:
+        if n in out:
+            continue
         like = arrays.get(n)
         if (inplace and like is not None and marshal.kind_of(like) == "torch" and like.is_cuda
                 and words[n].data_ptr() == like.data_ptr()):
             out[n] = like
             continue
         k = marshal.kind_of(like) if like is not None else default_kind
-        out[n] = marshal.finish(plan, srcs.get(n), words[n], shapes[n], k, like)
+        out[n] = marshal.finish(plan, srcs.get(n), words[n], shapes[n], k, like, owned=owned)
     if rename:
         back = {v: k for k, v in rename.items()}
         out = {back.get(k, k): v for k, v in out.items()}

@@ -328,14 +328,15 @@ def device_words(pl: Plan, src: Source, count: int, device):
     return torch.from_numpy(host).to(device)
 
 
-def finish(pl: Plan, src: Source | None, words, shape, like_kind: str, like=None):
+def finish(pl: Plan, src: Source | None, words, shape, like_kind: str, like=None, owned: bool = False):
     """The caller-facing array for one program array.
 
     ``words``: flat numpy array (host) or torch tensor (device) holding the
     declared elements after the run.  Elements the caller supplied beyond the
     declared extent are returned unchanged; the container is the caller's
     (list / numpy / torch on the caller's device), numpy and torch arrays in
-    ``pl.out_dtype`` (the caller's dtype for the permutations).
+    ``pl.out_dtype`` (the caller's dtype for the permutations).  ``owned``:
+    ``words`` is a fresh host array this call may hand out without a copy.
     """
     count = 1
     for d in shape:
@@ -377,8 +378,75 @@ def finish(pl: Plan, src: Source | None, words, shape, like_kind: str, like=None
             return host.tolist() + list(tail)
         return np.concatenate([host, np.asarray(tail).astype(host.dtype)])
     if like_kind == "numpy":
-        return host.reshape(shape).copy()
+        return host.reshape(shape) if owned else host.reshape(shape).copy()
     return host.reshape(shape).tolist()
+
+
+def copy_input(pl: Plan, src: Source | None, shape, like_kind: str, like=None):
+    """The caller-facing value of an array the program never writes: a copy
+    of what the caller supplied (interp.py:183-186 deep-copies inputs), in
+    the dtype finish() would return it in, without a device round trip.
+    Lists come back as lists of the very same objects (an int stays an int
+    even when the run computes in binary64)."""
+    import torch
+
+    count = 1
+    for d in shape:
+        count *= d
+    if src is None:
+        if like_kind == "list":
+            return [[0] * shape[1] for _ in range(shape[0])] if len(shape) == 2 else [0] * shape[0]
+        dt = pl.default_out if pl.default_out is not None else pl.np_dtype
+        if like_kind == "numpy":
+            return np.zeros(shape, dtype=dt)
+        return torch.zeros(shape, dtype=_torch_out_dtype(dt))
+    if src.kind == "list":
+        v = src.value
+        return [list(r) for r in v] if v and isinstance(v[0], (list, tuple)) else list(v)
+    out_dt = pl.out_dtype.get(src.name) or pl.np_dtype
+    if pl.objects:
+        out_dt = None
+    if src.kind == "numpy":
+        a = src.value
+        if out_dt is not None and a.dtype != out_dt:
+            return a.astype(out_dt)
+        return fresh_copy(a)
+    t = src.value.detach()
+    if out_dt is not None and t.dtype != _torch_out_dtype(out_dt):
+        return t.to(_torch_out_dtype(out_dt))
+    return t.clone()
+
+
+def _par_copy_types():
+    import torch
+
+    return {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+            np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64, np.dtype(np.int16): torch.int16,
+            np.dtype(np.int8): torch.int8, np.dtype(np.uint8): torch.uint8, np.dtype(np.float16): torch.float16}
+
+
+class _LazyTypes(dict):
+    def get(self, k, default=None):
+        if not self:
+            self.update(_par_copy_types())
+        return super().get(k, default)
+
+
+_PAR_COPY = _LazyTypes()
+
+
+def fresh_copy(words: np.ndarray) -> np.ndarray:
+    """A fresh host array with the contents of ``words`` (e.g. a pinned
+    staging buffer), copied by torch's threads (page-faulting fresh memory is
+    the slow part of a large copy)."""
+    import torch
+
+    td = _PAR_COPY.get(words.dtype)
+    if words.size < (1 << 16) or td is None or not words.flags.c_contiguous:
+        return words.copy()
+    out = torch.empty(words.shape, dtype=td).numpy()
+    torch.from_numpy(out).copy_(torch.from_numpy(words))
+    return out
 
 
 def _as_kind(vals: list, shape, like_kind: str, _dt):

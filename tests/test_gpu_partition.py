@@ -300,3 +300,29 @@ def test_launch_multi_fewer_units_than_devices(cuda, oracle_mod, family, params,
     got = run_program(programs.source(family), params, init, devices=[0] * ndev)
     for name in shapes:
         assert np.array_equal(np.asarray(got[name]).reshape(-1), np.asarray(want[name]).reshape(-1)), name
+
+
+@pytest.mark.parametrize("family,params", [
+    ("jacobi", {"T": 501, "N": (1 << 20) + 2, "s": 4, "B": 256}),
+    ("jacobi2d", {"T": 500, "N": 1026, "s": 4, "B0": 8, "B1": 32}),
+])
+@pytest.mark.parametrize("ndev", [2, 4])
+def test_fused_peer_sweeps_under_real_concurrency(cuda, family, params, ndev):
+    """pk_launch_multi's fused sweep with every "device" a separate stream on
+    the one GPU: the devices' kernels run truly concurrently (unlike separate
+    processes, which time-slice), so the edge blocks' waits and signals race
+    the neighbours' stores for hundreds of steps.  Bit-identical to one
+    pk_launch of the whole program."""
+    torch = cuda
+    from paper_1801_04348_b200 import programs, run_program
+
+    N = params["N"]
+    n = 2 * N if family == "jacobi" else 2 * N * N
+    g = torch.Generator(device="cuda").manual_seed(ndev)
+    a = torch.randint(-(1 << 20), 1 << 20, (n,), dtype=torch.int32, device="cuda", generator=g)
+    if family == "jacobi2d":
+        a = a.view(2 * N, N)
+    want = run_program(programs.source(family), params, {"a": a})["a"]
+    for _ in range(3):
+        got = run_program(programs.source(family), params, {"a": a}, devices=[0] * ndev)["a"]
+        assert torch.equal(got.reshape(-1), want.reshape(-1))

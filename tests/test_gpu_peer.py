@@ -96,3 +96,15 @@ def test_peer_stencil_wide_values(cuda, oracle_mod, tmp_path):
     init, got = _run(tmp_path, "jacobi2d", params, 2, False, 2**31 - 1)
     want = oracle_mod.run("jacobi2d", params, {"a": init.reshape(2 * params["N"], -1)})
     assert np.array_equal(got.reshape(-1), np.asarray(want["a"]).reshape(-1))
+
+
+@pytest.mark.parametrize("family,params", [
+    ("jacobi", {"T": 600, "N": 20002, "s": 4, "B": 64}),
+    ("jacobi2d", {"T": 500, "N": 130, "s": 2, "B0": 8, "B1": 16}),
+])
+def test_peer_stencil_long_runs(cuda, oracle_mod, tmp_path, family, params):
+    """PeerStencil for hundreds of steps (2 processes): the counters keep the
+    edge blocks in step through T >= 500 exchanges."""
+    init, got = _run(tmp_path, family, params, 2, True, 1 << 20)
+    want = oracle_mod.run(family, params, {"a": init if family == "jacobi" else init.reshape(2 * params["N"], -1)})
+    assert np.array_equal(got.reshape(-1), np.asarray(want["a"]).reshape(-1))
