@@ -84,17 +84,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 #ifndef PK_MM_GROUP
-#define PK_MM_GROUP 8
+#define PK_MM_GROUP 16
 #endif
 
-// Tile t of the grouped raster: tiles launched together cover a GROUP x
-// (all columns) band walked column-group by column-group, so the a rows and
-// b columns a wave touches stay resident in L2.
-__device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int &m0, int &n0) {
-    constexpr int GROUP = PK_MM_GROUP;
-    const int per_group = GROUP * ntn;
-    const int g = t / per_group, first = g * GROUP;
-    const int gsize = min(ntm - first, GROUP);
+// Tile t of the grouped raster: tiles in flight together cover a GROUP x
+// (some columns) block of the tile grid walked column by column, so the a
+// row panels and b column panels a wave streams through k are shared by
+// GROUP (resp. P / GROUP) CTAs at once -- DRAM reads per wave ~ (GROUP +
+// P / GROUP) panels, least near GROUP = sqrt(P).
+__device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, int &m0, int &n0) {
+    const int per_group = group * ntn;
+    const int g = t / per_group, first = g * group;
+    const int gsize = min(ntm - first, group);
     const int local = t - g * per_group;
     m0 = (first + local % gsize) * BM;
     n0 = (local / gsize) * BN;
@@ -193,37 +194,53 @@ __device__ __forceinline__ void mm_init(unsigned char *&smem, uint64_t *&full, u
 __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
                                                           const __grid_constant__ CUtensorMap map_b,
                                                           float *__restrict__ C, int64_t ldc, int64_t rlo,
-                                                          int ntn, int ktiles) {
+                                                          int ntn, int ktiles, int group) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem;
     uint64_t *full, *empty;
     mm_init(smem, full, empty, smem_raw);
     int m0, n0, gs = 0;
-    tile_origin(blockIdx.x, (int)(gridDim.x / ntn), ntn, m0, n0);
+    tile_origin(blockIdx.x, (int)(gridDim.x / ntn), ntn, group, m0, n0);
     mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
 }
 
 // Persistent CTAs over an order-preserving split of the work (see
-// mm_schedule): CTA p runs its items in order; an item that continues a
-// tile's reduction waits until the part before it has stored c (the tile's
-// progress word equals its first slab), and every item publishes its last
-// slab after storing.  c is the fp32 accumulator between the parts, so the
-// bits equal one launch.  Items: {tile, first slab, end slab}; CTA p owns
-// items [off[p], off[p+1]).
+// mm_schedule).  Phase 1: whole tiles [0, base) handed out in raster order by
+// a ticket counter, so the tiles in flight are always a contiguous window of
+// the grouped raster (L2 reuse as in a plain grid; static assignment let fast
+// CTAs drift ahead and scatter the window).  Phase 2: the CTA's own items
+// {tile, first slab, end slab} [off[p], off[p+1]) -- the tail waves cut into
+// equal runs; an item that continues a tile's reduction waits until the part
+// before it has stored c (the tile's progress word equals its first slab),
+// and every item publishes its last slab after storing.  c is the fp32
+// accumulator between the parts, so the bits equal one launch.
 __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_constant__ CUtensorMap map_at,
                                                                 const __grid_constant__ CUtensorMap map_b,
                                                                 float *__restrict__ C, int64_t ldc, int64_t rlo,
-                                                                int ntm, int ntn, const int3 *__restrict__ items,
-                                                                const int *__restrict__ off, int *progress) {
+                                                                int ntm, int ntn, int group, int base, int ktiles,
+                                                                const int3 *__restrict__ items,
+                                                                const int *__restrict__ off, int *progress,
+                                                                int *ticket) {
     extern __shared__ unsigned char smem_raw[];
+    __shared__ int next;
     unsigned char *smem;
     uint64_t *full, *empty;
     mm_init(smem, full, empty, smem_raw);
     int gs = 0;
+    for (;;) {
+        if (threadIdx.x == 0) next = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int t = next;
+        __syncthreads();  // every thread has read next before thread 0 overwrites it
+        if (t >= base) break;
+        int m0, n0;
+        tile_origin(t, ntm, ntn, group, m0, n0);
+        mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
+    }
     for (int it = off[blockIdx.x]; it < off[blockIdx.x + 1]; it++) {
         const int3 w = items[it];
         int m0, n0;
-        tile_origin(w.x, ntm, ntn, m0, n0);
+        tile_origin(w.x, ntm, ntn, group, m0, n0);
         if (w.y > 0) {  // the tile's slabs before w.y are another CTA's: wait for their c
             if (threadIdx.x == 0) {
                 int v;
@@ -304,17 +321,17 @@ struct DevSched {
 std::mutex g_sched_mu;
 std::map<std::tuple<int, int64_t, int64_t, int>, DevSched> g_sched;  // (device, T, KS, P)
 
+// All but the last 1-2 waves are whole tiles handed out by the kernel's
+// ticket counter (tiles [0, base)); the rest are split into P equal runs of
+// >= one tile (so a tile is cut at most once and its second part never waits
+// in practice).
+int64_t schedule_base(int64_t T, int P) { return (T / P >= 2 ? T / P - 1 : 0) * P; }
+
 int build_schedule(int64_t T, int64_t KS, int P, std::vector<int3> &items, std::vector<int> &off) {
-    // all but the last 1-2 waves as whole tiles in raster order (CTA p takes
-    // tile w*P + p at step w, the tiles running together stay L2 neighbours),
-    // the rest split into equal runs of >= one tile (so a tile is cut at most
-    // once and its second part never waits in practice)
-    const int64_t W0 = T / P >= 2 ? T / P - 1 : 0;
-    const int64_t base = W0 * P, S = (T - base) * KS;
+    const int64_t base = schedule_base(T, P), S = (T - base) * KS;
     off.assign(P + 1, 0);
     for (int p = 0; p < P; p++) {
         off[p] = (int)items.size();
-        for (int64_t w = 0; w < W0; w++) items.push_back(make_int3((int)(w * P + p), 0, (int)KS));
         const int64_t s0 = S * p / P, s1 = S * (p + 1) / P;
         if (s1 <= s0) continue;
         const int64_t t0 = s0 / KS, t1 = (s1 - 1) / KS;
@@ -372,6 +389,9 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
             (rc = allow_smem((const void *)k_matmul_tma_sched, SMEM_BYTES)) == PK_OK) {
             const int ntn = (int)(Nc / BN), ntm = (int)(rows / BM);
             const int64_t T = (int64_t)ntm * ntn, KS = K / BK;
+            // rows of tiles per raster group (PK_MM_GROUP overrides: tuning aid)
+            const char *genv = getenv("PK_MM_GROUP");
+            const int group = genv && atoi(genv) > 0 ? atoi(genv) : PK_MM_GROUP;
             // persistent split when the tiles leave the last wave part-empty
             int dev = 0, sms = 0, per_sm = 0;
             cudaGetDevice(&dev);
@@ -382,20 +402,21 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
                                T * KS < ((int64_t)1 << 31);
             if (split) {
                 DevSched d;
-                int *progress = nullptr;
+                int *progress = nullptr;  // T progress words, then the ticket counter
                 if ((rc = schedule_for(dev, T, KS, (int)P, &d)) == PK_OK) {
-                    e = scratch_alloc((void **)&progress, (size_t)T * sizeof(int), st);
+                    e = scratch_alloc((void **)&progress, (size_t)(T + 1) * sizeof(int), st);
                     if (e != cudaSuccess) rc = fail(PK_E_ALLOC, "matmul progress words: %s", cudaGetErrorString(e));
                 }
                 if (rc == PK_OK) {
-                    cudaMemsetAsync(progress, 0, (size_t)T * sizeof(int), st);
-                    k_matmul_tma_sched<<<(unsigned)P, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntm, ntn,
-                                                                                  d.items, d.off, progress);
+                    cudaMemsetAsync(progress, 0, (size_t)(T + 1) * sizeof(int), st);
+                    k_matmul_tma_sched<<<(unsigned)P, NTHREADS, SMEM_BYTES, st>>>(
+                        mat, mb, c, n, rlo, ntm, ntn, group, (int)schedule_base(T, (int)P), (int)KS, d.items, d.off,
+                        progress, progress + T);
                     rc = after_launch("matmul_tma_sched");
                     cudaFreeAsync(progress, st);
                 }
             } else {
-                k_matmul_tma<<<(unsigned)T, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn, (int)KS);
+                k_matmul_tma<<<(unsigned)T, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn, (int)KS, group);
                 rc = after_launch("matmul_tma");
             }
         }

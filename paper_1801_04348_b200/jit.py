@@ -365,20 +365,30 @@ def run_program_jit(leaf: Leaf, params: dict, arrays: dict | None = None):
     import numpy as np
     import torch
 
+    from .interp import _to_device_tensor
+
     arrays = arrays or {}
     shapes = array_shapes(leaf, params)
     bufs = {}
+    dev = torch.device("cuda", torch.cuda.current_device())
     for name, shape in shapes.items():
         n = eval_product(shape)
         if name in arrays:
-            host = np.ascontiguousarray(np.asarray(arrays[name], dtype=np.int64).reshape(-1)[:n], dtype=np.int32)
-            bufs[name] = torch.from_numpy(host.copy()).cuda()
+            # the emitted leaves carry no bounds guards: an array shorter than
+            # its declaration raises IndexError here (interp.py:209-212) instead
+            # of letting the kernel run past the buffer; values outside int32
+            # raise OverflowError instead of wrapping
+            t, _ = _to_device_tensor(name, arrays[name], shape, np.int32, dev)
+            bufs[name] = t[: max(n, 1)].contiguous() if t.numel() > n else t
         else:
             bufs[name] = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
     run_leaf(leaf, params, bufs, stream)
     torch.cuda.synchronize()
     out = {}
+    for name, v in arrays.items():  # arrays the program does not declare come back as copies
+        if name not in shapes:
+            out[name] = v.copy() if isinstance(v, np.ndarray) else [r[:] if isinstance(r, list) else r for r in v]
     for name, shape in shapes.items():
         host = bufs[name].cpu().numpy()[: eval_product(shape)].reshape(shape)
         out[name] = host.tolist() if not isinstance(arrays.get(name), np.ndarray) else host

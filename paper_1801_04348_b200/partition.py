@@ -425,11 +425,19 @@ def pk_launcher(family: str, P: dict, arrays: dict, *, machine=None, dtype=None,
 
     from . import _lib, binding, cases
 
+    from . import machine as machine_mod
+
     kind = programs.original(family)
-    sel = cases.select(kind, P, machine)
     names = [a.name for a in programs.FAMILIES[family].arrays]
     if dtype is None:
-        dtype = _lib.DTYPE_F32 if arrays[names[0]].dtype == torch.float32 else _lib.DTYPE_I32
+        dtype = {torch.float32: _lib.DTYPE_F32, torch.float64: _lib.DTYPE_F64,
+                 torch.int64: _lib.DTYPE_I64}.get(arrays[names[0]].dtype, _lib.DTYPE_I32)
+    if machine is None:  # this rank's own device (not device 0): selection on the GPU that runs the leaf
+        dev = arrays[names[0]].device
+        elem = 8 if dtype in (_lib.DTYPE_F64, _lib.DTYPE_I64) else 4
+        machine = machine_mod.live(dev.index if dev.type == "cuda" else torch.cuda.current_device(),
+                                   elem_bytes=elem)
+    sel = cases.select(kind, P, machine)
 
     def launch(lo, hi):
         L = binding.make_launch(kind, P, sel.applied, dtype, lo=lo, hi=hi)

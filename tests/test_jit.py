@@ -75,3 +75,23 @@ def test_block_leaf_pins_every_grid_loop():
             for var, _ in leaf.grid:
                 assert "int pk_rb_%s" % var in b.source
                 assert ("pk_rb_%s" % var, "int") in b.args
+
+
+@pytest.mark.gpu
+def test_emitted_path_refuses_short_and_wide_arrays(cuda):
+    """The emitted leaves have no bounds guards: run_program_jit raises
+    IndexError for an array shorter than declared (interp.py:209-212) and
+    OverflowError for values outside int32, instead of running past the
+    buffer or wrapping; undeclared arrays come back as copies."""
+    e = next(x for x in _entries() if x["program"] == "saxpy" and x["variant"] == "original")
+    leaf = jit.Leaf.from_json(e["leaf"])
+    v = e["vectors"][0]
+    short = {k: (d[:-1] if not (d and isinstance(d[0], list)) else d[:-1]) for k, d in v["inputs"].items()}
+    with pytest.raises(IndexError):
+        jit.run_program_jit(leaf, v["params"], short)
+    wide = {k: [[2**40] * len(d[0])] * len(d) if d and isinstance(d[0], list) else [2**40] * len(d)
+            for k, d in v["inputs"].items()}
+    with pytest.raises(OverflowError):
+        jit.run_program_jit(leaf, v["params"], wide)
+    got = jit.run_program_jit(leaf, v["params"], dict(v["inputs"], extra=[7]))
+    assert got["extra"] == [7]
