@@ -46,6 +46,13 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found (CUDA 12.9 toolkit expected at /usr/local/cuda)")
 
 
+# per-file extra flags: k_matvec.cu's packed double-float sums (FMUL2 / FADD2)
+# must not be contracted into FFMA2 by ptxas -- the TwoSum needs the rounded
+# product (the scalar path's __fmul_rn / __fadd_rn intrinsics are immune, the
+# f32x2 instructions are not)
+FILE_FLAGS = {"k_matvec.cu": ["--fmad=false", "-Xptxas", "--fmad=false"]}
+
+
 def sources() -> list[str]:
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
@@ -60,7 +67,7 @@ def _compile(src: str, log_dir: str) -> str:
         )
         if os.path.getmtime(obj) >= newest_dep:
             return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(log_dir, os.path.basename(src) + ".ptxas.txt"), "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)

@@ -42,9 +42,73 @@ __global__ void __launch_bounds__(256) k_addition(const T *__restrict__ a, const
     }
 }
 
+// 16-byte vectors of V = 16 / sizeof(T) elements.  Vector u of the run is
+// column vector w = u % per_row of row rlo + u / per_row, where a row holds
+// [0, Jv) and, for the twin form, [halfv, halfv + Jv); when the covered
+// columns are the whole row the rows are one contiguous run (per_row = 0
+// selects that form: vector u at rlo*N/V + u).  Each thread keeps U vectors
+// of a and b in flight.
+template <typename T>
+__device__ __forceinline__ int4 add_vec(const int4 &x, const int4 &y) {
+    int4 r;
+    const T *xs = reinterpret_cast<const T *>(&x), *ys = reinterpret_cast<const T *>(&y);
+    T *rs = reinterpret_cast<T *>(&r);
+#pragma unroll
+    for (int i = 0; i < (int)(16 / sizeof(T)); i++) rs[i] = add_elem(xs[i], ys[i]);
+    return r;
+}
+
+constexpr int kAddThreads = 256, kAddU = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(kAddThreads) k_addition_vec(const int4 *__restrict__ a, const int4 *__restrict__ b,
+                                                             int4 *__restrict__ c, int64_t Nv, int64_t rlo,
+                                                             int64_t Jv, int64_t halfv, int64_t per_row,
+                                                             int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * kAddThreads;
+    for (int64_t u0 = (int64_t)blockIdx.x * kAddThreads * kAddU + threadIdx.x; u0 < total;
+         u0 += stride * kAddU) {
+        int64_t off[kAddU];
+        int4 x[kAddU], y[kAddU];
+#pragma unroll
+        for (int k = 0; k < kAddU; k++) {
+            const int64_t u = u0 + (int64_t)k * kAddThreads;
+            if (per_row == 0) {
+                off[k] = rlo * Nv + u;
+            } else {
+                const int64_t r = u / per_row, w = u - r * per_row;
+                off[k] = (rlo + r) * Nv + (w < Jv ? w : halfv + (w - Jv));
+            }
+            if (u < total) {
+                x[k] = ld_stream(a + off[k]);
+                y[k] = ld_stream(b + off[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kAddU; k++)
+            if (u0 + (int64_t)k * kAddThreads < total) st_stream(c + off[k], add_vec<T>(x[k], y[k]));
+    }
+}
+
 template <typename T>
 void launch_t(void *const *p, int64_t N, int64_t rlo, int64_t rhi, int64_t J, int64_t half, bool merged,
               int64_t span, cudaStream_t st) {
+    constexpr int V = 16 / sizeof(T);
+    if (N % V == 0 && J % V == 0 && half % V == 0 && aligned16(p[0]) && aligned16(p[1]) && aligned16(p[2])) {
+        const int64_t Jv = J / V, halfv = half / V, Nv = N / V, rows = rhi - rlo;
+        const bool whole = merged ? J == N : (J == half && 2 * half == N);
+        const int64_t per_row = whole ? 0 : (merged ? Jv : 2 * Jv);
+        const int64_t total = rows * (whole ? Nv : per_row);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int64_t blocks = ceil_div(total, (int64_t)kAddThreads * kAddU);
+        if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;  // persistent-style grid stride
+        k_addition_vec<T><<<(unsigned)blocks, kAddThreads, 0, st>>>(
+            static_cast<const int4 *>(p[0]), static_cast<const int4 *>(p[1]), static_cast<int4 *>(p[2]), Nv, rlo,
+            Jv, halfv, per_row, total);
+        return;
+    }
     const int nt = 256;
     int64_t gx = ceil_div(span, nt);
     if (gx > 4096) gx = 4096;

@@ -41,12 +41,63 @@ __device__ __forceinline__ void df_add_prod(DF &acc, float a, float x) {
     df_add(acc, p, __fmaf_rn(a, x, -p));  // p + fma(a, x, -p) == a * x exactly
 }
 
+// The same double-float sum on packed pairs (sm_100 FADD2 / FMUL2 / FFMA2:
+// two IEEE fp32 operations per instruction): lane 0 accumulates the even
+// elements of a row, lane 1 the odd ones, so every 16-byte load of a is two
+// exact products and two TwoSums in 11 instructions instead of 20.
+struct DF2 {
+    unsigned long long hi, lo;  // {even, odd} halves
+};
+
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// acc += v (exactly, TwoSum per half) with err_in folded into the low parts
+__device__ __forceinline__ void df2_add(DF2 &acc, unsigned long long v, unsigned long long err_in) {
+    const unsigned long long t = add2(acc.hi, v);
+    const unsigned long long bp = sub2(t, acc.hi);
+    const unsigned long long err = add2(sub2(acc.hi, sub2(t, bp)), sub2(v, bp));
+    acc.hi = t;
+    acc.lo = add2(acc.lo, add2(err, err_in));
+}
+
+__device__ __forceinline__ void df2_add_prod(DF2 &acc, unsigned long long a, unsigned long long x) {
+    // the rounded products by two scalar mul.rn.f32: ptxas contracts a packed
+    // product (mul.rn.f32x2, or fma.rn.f32x2 with -0.0) and the TwoSum's
+    // add.rn.f32x2 into one FFMA2 even under --fmad=false, which would fold
+    // the product's rounding into the sum; scalar .rn products it leaves alone
+    const float p0 = __fmul_rn(__uint_as_float((unsigned)a), __uint_as_float((unsigned)x));
+    const float p1 = __fmul_rn(__uint_as_float((unsigned)(a >> 32)), __uint_as_float((unsigned)(x >> 32)));
+    const unsigned long long p = ((unsigned long long)__float_as_uint(p1) << 32) | __float_as_uint(p0);
+    const unsigned long long e = fma2(a, x, sub2(0ull, p));  // a*x - p exactly (halves of +0.0 - p)
+    df2_add(acc, p, e);
+}
+
 template <typename T> struct Acc;
 template <> struct Acc<int> { using type = int; };
-template <> struct Acc<float> { using type = DF; };
+template <> struct Acc<float> { using type = DF2; };
 
 __device__ __forceinline__ void acc_zero(int &a) { a = 0; }
 __device__ __forceinline__ void acc_zero(DF &a) { a.hi = a.lo = 0.f; }
+__device__ __forceinline__ void acc_zero(DF2 &a) { a.hi = a.lo = 0ull; }
 
 __device__ __forceinline__ int group_sum(int v, int lanes) {
     for (int o = lanes >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, lanes);
@@ -58,6 +109,28 @@ __device__ __forceinline__ DF group_sum(DF v, int lanes) {
         df_add(v, h, l);
     }
     return v;
+}
+
+__device__ __forceinline__ DF2 group_sum(DF2 v, int lanes) {
+    for (int o = lanes >> 1; o > 0; o >>= 1) {
+        const unsigned long long h = __shfl_xor_sync(0xffffffffu, v.hi, o, lanes);
+        const unsigned long long l = __shfl_xor_sync(0xffffffffu, v.lo, o, lanes);
+        df2_add(v, h, l);
+    }
+    return v;
+}
+__device__ __forceinline__ void dot4(DF2 &acc, const int4 &av, const float *xp) {
+    const unsigned long long *x2 = reinterpret_cast<const unsigned long long *>(xp);
+    df2_add_prod(acc, ((unsigned long long)(unsigned)av.y << 32) | (unsigned)av.x, x2[0]);
+    df2_add_prod(acc, ((unsigned long long)(unsigned)av.w << 32) | (unsigned)av.z, x2[1]);
+}
+__device__ __forceinline__ void dot1(DF2 &acc, float a, float x) {  // even half only
+    df2_add_prod(acc, (unsigned long long)__float_as_uint(a), (unsigned long long)__float_as_uint(x));
+}
+__device__ __forceinline__ float finish(float y, DF2 sum) {
+    const float h0 = __uint_as_float((unsigned)sum.hi), h1 = __uint_as_float((unsigned)(sum.hi >> 32));
+    const float l0 = __uint_as_float((unsigned)sum.lo), l1 = __uint_as_float((unsigned)(sum.lo >> 32));
+    return (float)((((double)y + (double)h0) + (double)h1) + ((double)l0 + (double)l1));
 }
 
 __device__ __forceinline__ void dot4(int &acc, const int4 &av, const int *xp) {
@@ -79,8 +152,14 @@ __device__ __forceinline__ float finish(float y, DF sum) {
     return (float)(((double)y + (double)sum.hi) + (double)sum.lo);
 }
 
+#ifndef PK_MV_FUNROLL
+#define PK_MV_FUNROLL 4
+#endif
 constexpr int kRows = 4;    // rows per lane group in flight
-constexpr int kUnroll = 4;  // 128-bit loads per row in flight
+// 128-bit loads per row in flight: 4 for int32; 3 for float32, whose packed
+// double-float accumulators (4 registers per row) would otherwise spill
+template <typename T> struct Unroll { static constexpr int value = 4; };
+template <> struct Unroll<float> { static constexpr int value = PK_MV_FUNROLL; };
 
 #ifndef PK_MV_NT
 #define PK_MV_NT 512
@@ -90,6 +169,7 @@ __global__ void __launch_bounds__(PK_MV_NT) k_matvec(const T *__restrict__ a, co
                                                 T *__restrict__ y, int64_t N, int64_t rlo,
                                                 int64_t rhi, int tile, int lanes) {
     using A = typename Acc<T>::type;
+    constexpr int kUnroll = Unroll<T>::value;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const T *xs = x;
     if (STAGED) {
