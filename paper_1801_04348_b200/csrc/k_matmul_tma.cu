@@ -6,6 +6,11 @@
 // * a's rows of this launch are transposed once (k_transpose_rows, ~1 % of
 //   the multiply at n = 8192) so both operands are plain 2-D boxes: the
 //   a^T slab BK x BM and the b slab BK x BN of k-step kt are one TMA each.
+//   PK_MM_ROWA=1 instead loads a's rows as they lie (128-byte swizzled
+//   [BM][BK] box, 8 scalar shared loads per k step): no transpose launch and
+//   0.5 GB less DRAM traffic, but measured 12 % slower (19.3 vs 17.0 ms at
+//   n = 8192: the extra loads spill at the 128-register budget), so it is
+//   off by default.
 // * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage;
 //   thread 0 also issues the TMAs (a separate producer warp would push the
 //   block past the 2-blocks-per-SM register budget); the 8 compute warps
@@ -41,6 +46,9 @@ constexpr int BM = 8 * TY, BN = 8 * TX;     // 128 x 128 block tile
 #endif
 #ifndef PK_MM_AHEAD
 #define PK_MM_AHEAD 1
+#endif
+#ifndef PK_MM_ROWA
+#define PK_MM_ROWA 0
 #endif
 constexpr int BK = PK_MM_BK;                // k slab per stage
 constexpr int STAGES = PK_MM_STAGES;
@@ -84,21 +92,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 #ifndef PK_MM_GROUP
-#define PK_MM_GROUP 16
+#define PK_MM_GROUP 8
 #endif
 
 // Tile t of the grouped raster: tiles in flight together cover a GROUP x
 // (some columns) block of the tile grid walked column by column, so the a
 // row panels and b column panels a wave streams through k are shared by
 // GROUP (resp. P / GROUP) CTAs at once -- DRAM reads per wave ~ (GROUP +
-// P / GROUP) panels, least near GROUP = sqrt(P).
+// P / GROUP) panels in lockstep.  Measured (ncu, n = 8192): the waves drift
+// out of k-lockstep, so panels live about a tile-time in L2 and the small
+// group wins: DRAM reads per launch 5.07 / 5.2 / 5.5 / 6.4 GB at GROUP 8 /
+// 12 / 16 / 20 with the split schedule, 3.50 / 3.43 / 3.48 / 3.82 GB without
+// it; the time is the same (FFMA-bound, 4 % of DRAM bandwidth).
 __device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, int &m0, int &n0) {
     const int per_group = group * ntn;
     const int g = t / per_group, first = g * group;
     const int gsize = min(ntm - first, group);
     const int local = t - g * per_group;
     m0 = (first + local % gsize) * BM;
-    n0 = (local / gsize) * BN;
+    // odd groups walk the columns right to left (boustrophedon), so a window
+    // straddling two groups shares the b panels at the turn
+    const int col = local / gsize;
+    n0 = ((g & 1) ? ntn - 1 - col : col) * BN;
 }
 
 // Slabs [kb, ke) of tile (m0, n0): c rows -> packed accumulators, the ring,
@@ -120,13 +135,20 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         fence_proxy_async();
         unsigned char *st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
+#if PK_MM_ROWA
+        tma_load_2d(st, map_at, &full[s], (kb + j) * BK, m0);  // a rows as they lie: [BM rows][BK], 128B swizzle
+#else
         tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);
+#endif
         tma_load_2d(st + A_SLAB, map_b, &full[s], n0, (kb + j) * BK);
     };
     if (tid == 0)
         for (int j = 0; j < AHEAD && j < nk; j++) produce(j);
 
     const int tx = tid % TX, ty = tid / TX;
+#if PK_MM_ROWA
+    const int apar = (ty & 1) << 2, arow = ty * 4 * 128;
+#endif
     float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
     const int64_t chalf = (int64_t)(BM / 2) * ldc;
     // accumulators as packed column pairs: acc[i][jp] = {c[i][2jp], c[i][2jp+1]}
@@ -146,13 +168,31 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         mbar_wait(&full[s], (g / STAGES) & 1);
         const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
+#if PK_MM_ROWA
+        const unsigned char *Ab = smem + s * STAGE_BYTES;
+#endif
 #pragma unroll
         for (int kk = 0; kk < BK; kk++) {
+#if PK_MM_ROWA
+            // a slab [BM rows][32 k] with the 128-byte swizzle: element (r, k) at
+            // r*128 + ((k/4) ^ (r%8))*16 + (k%4)*4.  This thread's rows ty*4+i
+            // and BM/2+ty*4+i have r%8 = (i | 4*(ty&1)); the two rows a warp
+            // reads per load are 4 apart, so they land in different banks
+            const int c = kk >> 2;
+            float af[8];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int chunk = (c ^ i ^ apar) << 4;
+                af[i] = *reinterpret_cast<const float *>(Ab + arow + i * 128 + chunk + (kk & 3) * 4);
+                af[4 + i] = *reinterpret_cast<const float *>(Ab + arow + (BM / 2 + i) * 128 + chunk + (kk & 3) * 4);
+            }
+#else
             const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
             const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
+            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#endif
             const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + tx * 4);
             const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + BN / 2 + tx * 4);
-            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const unsigned long long bp[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
             for (int i = 0; i < 8; i++) {
@@ -278,7 +318,7 @@ EncodeTiled encode_fn() {
 
 // rows x cols fp32 row-major, box box_rows x box_cols, no swizzle (plain row-major slab in smem)
 int make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
-             int box_rows) {
+             int box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
     EncodeTiled enc = encode_fn();
     if (!enc) return fail(PK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -286,7 +326,7 @@ int make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t cols, int6
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return PK_OK;
@@ -377,14 +417,19 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
                       int64_t K, cudaStream_t st) {
     const int64_t rows = rhi - rlo;
     float *at = nullptr;
+    int rc = PK_OK;
+    CUtensorMap mat, mb;
+#if PK_MM_ROWA
+    rc = make_map(&mat, a + rlo * n, rows, K, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+#else
     cudaError_t e = scratch_alloc((void **)&at, (size_t)rows * K * sizeof(float), st);
     if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul a^T workspace: %s", cudaGetErrorString(e));
-    int rc = PK_OK;
     k_transpose_rows<<<dim3((unsigned)(K / 32), (unsigned)(rows / 32)), 256, 0, st>>>(a + rlo * n, at, rows, K, n);
-    if ((rc = after_launch("matmul_transpose_a")) == PK_OK) {
-        CUtensorMap mat, mb;
-        if ((rc = make_map(&mat, at, K, rows, rows, BM, BK)) == PK_OK &&
-            (rc = make_map(&mb, b, K, Nc, n, BN, BK)) == PK_OK &&
+    rc = after_launch("matmul_transpose_a");
+    if (rc == PK_OK) rc = make_map(&mat, at, K, rows, rows, BM, BK);
+#endif
+    if (rc == PK_OK) {
+        if ((rc = make_map(&mb, b, K, Nc, n, BN, BK)) == PK_OK &&
             (rc = allow_smem((const void *)k_matmul_tma, SMEM_BYTES)) == PK_OK &&
             (rc = allow_smem((const void *)k_matmul_tma_sched, SMEM_BYTES)) == PK_OK) {
             const int ntn = (int)(Nc / BN), ntm = (int)(rows / BM);
@@ -404,7 +449,7 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
                 DevSched d;
                 int *progress = nullptr;  // T progress words, then the ticket counter
                 if ((rc = schedule_for(dev, T, KS, (int)P, &d)) == PK_OK) {
-                    e = scratch_alloc((void **)&progress, (size_t)(T + 1) * sizeof(int), st);
+                    cudaError_t e = scratch_alloc((void **)&progress, (size_t)(T + 1) * sizeof(int), st);
                     if (e != cudaSuccess) rc = fail(PK_E_ALLOC, "matmul progress words: %s", cudaGetErrorString(e));
                 }
                 if (rc == PK_OK) {
@@ -421,7 +466,7 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
             }
         }
     }
-    cudaFreeAsync(at, st);
+    if (at) cudaFreeAsync(at, st);
     return rc;
 }
 
