@@ -232,7 +232,7 @@ def summary(line: dict) -> dict:
     def verdict(p):
         if not p:
             return None
-        return "ok" if (p == "exact" or p.startswith("within")) else "FAIL"
+        return "ok" if (p.startswith("exact") or p.startswith("within")) else "FAIL"
 
     out = {"cols": ["value", "unit", "frac_roofline", "cpu_port", "parity"],
            "matmul_n%d" % line["config"]["n"]: [line["value"], "GFLOP/s", line["roofline"]["frac"],
@@ -241,7 +241,7 @@ def summary(line: dict) -> dict:
     for fam, rec in (line.get("kernels") or {}).items():
         if not isinstance(rec, dict) or "value" not in rec or "temporal" in fam:
             continue
-        frac = rec.get("frac_of_measured_hbm", rec.get("frac_of_fp32_peak"))
+        frac = rec.get("frac_of_measured_hbm", rec.get("frac_of_fp32_peak", rec.get("frac_of_measured_hbm_x_n")))
         out[fam] = [rec["value"], rec["unit"], frac, (rec.get("cpu_baseline") or {}).get("value"),
                     verdict(rec.get("parity"))]
     if line.get("e2e"):
@@ -290,6 +290,12 @@ def main() -> int:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one collective now, so the communicator exists (and is logged) before any timing
+        probe = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(probe)
+        print("bench: rank %d of %d on cuda:%d, backend %s, communicator ranks %d (all_reduce check %d)"
+              % (rank, world, local, dist.get_backend(), dist.get_world_size(), int(probe.item())),
+              file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     peaks = load_peaks()
     mv = machine_mod.live(local)
@@ -866,6 +872,27 @@ def cpu_matmul_rows(n: int, r0: int, r1: int, threads: int) -> dict:
                       "%.3f s/run x %d" % (n, r0, r1, flop, sec, runs)}
 
 
+def _owned_slices(fam: str, P: dict, lo: int, hi: int) -> list:
+    """(array index, start, end) of the flat elements units [lo, hi) write --
+    a rank's share of the result."""
+    from paper_1801_04348_b200 import partition, programs
+
+    if hi <= lo:
+        return []
+    if fam == "jacobi":
+        N = P["N"]
+        return [(0, lo, hi), (0, N + lo, N + hi)]
+    if fam == "jacobi2d":
+        N = P["N"]
+        return [(0, lo * N, hi * N), (0, (N + lo) * N, (N + hi) * N)]
+    names = [a.name for a in programs.FAMILIES[fam].arrays]
+    out = []
+    for w in programs.FAMILIES[fam].written:
+        off, cnt = partition.share_range(fam, P, w, lo, hi)
+        out.append((names.index(w), off, off + cnt))
+    return out
+
+
 def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
     """The bandwidth-bound BASELINE configs over all ranks (N > 1), placed by
     the partitioner: reversal by input element, transpose / mat-vec by output
@@ -936,6 +963,27 @@ def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
                         "value": round(gbs, 1), "unit": unit, "n_gpus": world,
                         "frac_of_measured_hbm_x_n": round(gbs / (peaks["hbm_gbs"] * world), 4),
                         "placement": detail if rank == 0 else None}
+            # parity of this rank's share at full size (outside the timed region):
+            # fresh inputs, one run, the written share against restate()
+            g.manual_seed(0x1801)
+            fresh = _fill(fam, shapes, g)
+            want = restate(fam, run_params, fresh)
+            for b, f in zip(bufs, fresh):
+                b.copy_(f)
+            del fresh
+            if fam in ("jacobi", "jacobi2d"):
+                run()
+                owned = _owned_slices(fam, run_params, plan.lo, plan.hi)
+            else:
+                if hi > lo:
+                    _lib.launch(L, ptrs, st.cuda_stream)
+                owned = _owned_slices(fam, run_params, lo, hi)
+            torch.cuda.synchronize()
+            ok = all(torch.equal(bufs[i][o0:o1], want[i][o0:o1]) for i, o0, o1 in owned)
+            ok_t = torch.tensor([0 if ok else 1], device=dev)
+            dist.all_reduce(ok_t, op=dist.ReduceOp.MAX)
+            out[fam]["parity"] = "exact (every rank's share)" if int(ok_t.item()) == 0 else "MISMATCH"
+            del want
             if fam in ("jacobi", "jacobi2d"):
                 # the same slabs with the halo exchange fused into the sweep: ghost units
                 # stored straight into the neighbours' buffers over NVLink (CUDA IPC), no NCCL
@@ -946,6 +994,8 @@ def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
                 ps.run(params["T"])  # warm-up
                 ps.finish()
                 ps.ctr.zero_()
+                g.manual_seed(0x1801)  # the timed run starts from fresh inputs (checked below)
+                bufs[0].copy_(_fill(fam, shapes, g)[0])
                 torch.cuda.synchronize()
                 dist.barrier()
                 e0.record(st)
@@ -953,6 +1003,16 @@ def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
                     _lib.jacobi_sweep_peer(L, bufs[0].data_ptr(), t, ps.lo, ps.hi, ps.peer, st.cuda_stream)
                 e1.record(st)
                 torch.cuda.synchronize()
+                # the timed run started from the fresh inputs: check this rank's slab
+                g.manual_seed(0x1801)
+                init = _fill(fam, shapes, g)
+                want = restate(fam, run_params, init)
+                del init
+                ps_ok = all(torch.equal(bufs[0][o0:o1], want[0][o0:o1])
+                            for _, o0, o1 in _owned_slices(fam, run_params, ps.lo, ps.hi))
+                del want
+                ok_t = torch.tensor([0 if ps_ok else 1], device=dev)
+                dist.all_reduce(ok_t, op=dist.ReduceOp.MAX)
                 ps.close()
                 pms = torch.tensor([e0.elapsed_time(e1)], device=dev)
                 dist.all_reduce(pms, op=dist.ReduceOp.MAX)
@@ -960,6 +1020,7 @@ def bench_kernels_sharded(peaks, mv, rank: int, world: int) -> dict:
                 pg = work / (pms * 1e-3) / 1e9
                 out[fam + "_peer"] = {"params": run_params, "ms": round(pms, 3), "value": round(pg, 1), "unit": unit,
                                       "n_gpus": world, "frac_of_measured_hbm_x_n": round(pg / (peaks["hbm_gbs"] * world), 4),
+                                      "parity": "exact (every rank's slab)" if int(ok_t.item()) == 0 else "MISMATCH",
                                       "exchange": "fused into the sweep: ghost units stored into the neighbours' "
                                                   "buffers through CUDA IPC (NVLink), device counters, no NCCL"}
             del bufs
