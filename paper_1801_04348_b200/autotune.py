@@ -8,6 +8,8 @@ times candidate assignments on the device and keeps the fastest, subject to:
    parameters write (``programs.coverage``), so results are unchanged;
 2. a case of the discussion holds at the live machine values (no fallback),
    and, with ``same_case=True``, it is the case the caller's point selects;
+   only the leaves that survive at the live machine (cases.surviving, the
+   reference's _machine_feasible pattern) are evaluated;
 3. the executor-side warp rule the reference cannot express (no warp-size
    machine parameter, counters.py:66): threads per block a multiple of the
    live warp size.
@@ -46,7 +48,9 @@ def candidates(family: str, base: dict, mv, *, same_case: bool = False, grid=Non
     """Parameter assignments that keep coverage and select a real case."""
     grid = grid or GRID[family]
     want = programs.coverage(family, base)
-    base_case = cases.select(family, base, mv).index if same_case else None
+    # a7 survival: leaves proven unable to hold at this machine are never evaluated
+    alive = {c.index for c in cases.surviving(family, mv, budget=20_000, maybe=True)}
+    base_case = cases.select(family, base, mv, among=alive).index if same_case else None
     if isinstance(grid, dict):
         keys = sorted(grid)
         points = [dict(zip(keys, combo)) for combo in itertools.product(*(grid[k] for k in keys))]
@@ -63,7 +67,7 @@ def candidates(family: str, base: dict, mv, *, same_case: bool = False, grid=Non
             continue
         if programs.threads_per_block(family, P) % mv.warp_size:
             continue
-        sel = cases.select(family, P, mv)
+        sel = cases.select(family, P, mv, among=alive)
         if sel.fallback or (base_case is not None and sel.index != base_case):
             continue
         out.append((P, sel))

@@ -144,3 +144,31 @@ def test_occupancy_target_range_and_warp_slots_checked():
     with pytest.raises(KeyError):
         cases.select("jacobi", {"T": 4, "N": 4098, "s": 2, "B": 256},
                      machine.MachineValues("b200-occ", machine.nominal().values, "user"))
+
+
+def test_surviving_leaves_match_reference_consistency_checker():
+    """a7: the leaves that can hold once the machine is fixed -- our
+    restatement of check_consistency against the reference's own verdicts
+    (tests/golden/survival.json, make_survival.py)."""
+    import json
+    import os
+    from fractions import Fraction
+
+    from paper_1801_04348_b200 import cases, machine
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "survival.json")
+    with open(path) as fh:
+        tables = json.load(fh)["tables"]
+    models = {"b200": machine.nominal(), "b200-static": machine.nominal(smem="static"),
+              "b200-occ": machine.nominal(occupancy=Fraction(1, 2)), "fermi": machine.fermi()}
+    checked = 0
+    for t in tables:
+        got = cases.surviving(t["family"], models[t["model"]], all_leaves=True)
+        assert [(s.case.index, s.status) for s in got] == [(v["case"], v["status"]) for v in t["verdicts"]], \
+            (t["family"], t["model"])
+        for s in got:  # a witness really satisfies the leaf at the fixed machine values
+            if s.status == "consistent":
+                point = dict(s.witness, **{k: Fraction(v) for k, v in t["values"].items()})
+                assert s.case.holds(point)
+        checked += 1
+    assert checked >= 28

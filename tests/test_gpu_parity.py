@@ -407,3 +407,17 @@ def test_matvec_float32_double_float_accumulation(cuda, N, scale):
     mag = y[:R].double().abs() + a[:R].double().abs() @ x.double().abs()
     err = (got[:R].double() - want).abs()
     assert bool((err <= 2.0 * 2.0**-24 * want.abs() + 2.0**-40 * mag).all())
+
+
+def test_surviving_leaves_on_live_device(cuda):
+    """a7 on the device itself: the live values leave the register-starved
+    leaves (R_B below the estimate) dead, and selection restricted to the
+    survivors picks the same leaf as the full evaluation."""
+    from paper_1801_04348_b200 import cases, live_machine
+
+    mv = live_machine()
+    alive = {f: [c.index for c in cases.surviving(f, mv)] for f in ("reverse", "matvec", "matmul", "jacobi")}
+    assert alive == {"reverse": [1, 3], "matvec": [1, 3], "matmul": [1, 3, 4], "jacobi": [1, 4]}
+    for P in ({"n": 8192, "B0": 128, "ub1": 8, "s": 16}, {"n": 512, "B0": 256, "ub1": 4, "s": 64}):
+        full = cases.select("matmul", P, mv)
+        assert cases.select("matmul", P, mv, among=set(alive["matmul"])).index == full.index
