@@ -69,7 +69,9 @@ extern "C" {
                           operation in the interpreter's order (no contraction): bit-identical
                           to interp.py on Python floats                                              */
 /* dtypes per family: reverse/transpose/addition/matvec/matmul take all four;
-   the Jacobi stencils take PK_DTYPE_I32.  Buffers hold elements of the dtype's size. */
+   the Jacobi stencils take I32 (the register sweeps), I64 and F64 (per-step
+   sweeps; "/" is the reference's c_div on Python floats).  Buffers hold
+   elements of the dtype's size. */
 
 /*
  * One program invocation.  Parameters carry the names of the ORIGINAL
@@ -156,6 +158,16 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
 /* pk_run_host with element counts: PK_E_BOUNDS when a buffer is shorter than
  * what the run touches or copies (the declared extent of each array). */
 int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device);
+
+/* One thread block of the program (the reference's run_block,
+ * interp.py:228-249): grid[0..ngrid) the grid meta_for indices (outer
+ * first: reverse / jacobi / matvec i; transpose / jacobi2d / addition
+ * v0, v1; matmul i, j), ctx[0..nctx) the serial context loop variable
+ * (jacobi / jacobi2d t, matmul k); the thread loops are swept by one CUDA
+ * block in the program's own statement order, on any PK_DTYPE_*.  The
+ * caller checks the block's accesses against its arrays. */
+int pk_launch_block(const pk_launch_t *L, const int64_t *grid, int ngrid, const int64_t *ctx, int nctx,
+                    void *const *dev_ptrs, int nptrs, void *stream);
 
 /* One Jacobi sweep over an explicit position range, used by the slab
  * partitioner (one process per GPU).  src/dst point at the two halves (1-D:

@@ -61,6 +61,7 @@ EXPORTS = (
     "pk_run_host_checked",
     "pk_launch_multi",
     "pk_jacobi_sweep",
+    "pk_launch_block",
     "pk_jacobi_sweep_peer",
     "pk_ipc_export",
     "pk_ipc_open",
@@ -176,6 +177,10 @@ def load() -> ctypes.CDLL:
         lib.pk_launch_multi.argtypes = [ctypes.POINTER(PkLaunch), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int64, ctypes.c_int]
         lib.pk_launch_multi.restype = ctypes.c_int
+        lib.pk_launch_block.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.POINTER(vp),
+                                         ctypes.c_int, vp]
+        lib.pk_launch_block.restype = ctypes.c_int
         lib.pk_jacobi_sweep.argtypes = [ctypes.POINTER(PkLaunch), vp, vp, ctypes.c_int64, ctypes.c_int64, vp]
         lib.pk_jacobi_sweep.restype = ctypes.c_int
         lib.pk_jacobi_sweep_peer.argtypes = [ctypes.POINTER(PkLaunch), vp, ctypes.c_int64, ctypes.c_int64,
@@ -278,6 +283,14 @@ def launch_multi(L: PkLaunch, devices, ptr_lists, halo: int = 0, gather: bool = 
     flat = ptr_array([p for ptrs in ptr_lists for p in ptrs])
     nptrs = len(ptr_lists[0]) if ptr_lists else 0
     check(lib.pk_launch_multi(ctypes.byref(L), n, devs, flat, nptrs, int(halo), 1 if gather else 0))
+
+
+def launch_block(L: PkLaunch, grid, ctx, ptrs, stream: int = 0) -> None:
+    """pk_launch_block: one thread block at grid indices ``grid`` and context values ``ctx``."""
+    g = (ctypes.c_int64 * max(1, len(grid)))(*[int(v) for v in grid])
+    c = (ctypes.c_int64 * max(1, len(ctx)))(*[int(v) for v in ctx])
+    check(load().pk_launch_block(ctypes.byref(L), g, len(grid), c, len(ctx), ptr_array(ptrs), len(ptrs),
+                                 ctypes.c_void_p(stream or None)))
 
 
 def jacobi_sweep(L: PkLaunch, src: int, dst: int, lo: int, hi: int, stream: int = 0) -> None:

@@ -198,8 +198,8 @@ int dispatch(const pk_launch_t &L, void *const *p, cudaStream_t st) {
     switch (L.family) {
         case PK_FAMILY_REVERSE: return launch_reverse(L, p, st);
         case PK_FAMILY_TRANSPOSE: return launch_transpose(L, p, st);
-        case PK_FAMILY_JACOBI1D: return launch_jacobi1d(L, p, st);
-        case PK_FAMILY_JACOBI2D: return launch_jacobi2d(L, p, st);
+        case PK_FAMILY_JACOBI1D: return L.dtype == PK_DTYPE_I32 ? launch_jacobi1d(L, p, st) : launch_jacobi_wide(L, p, st);
+        case PK_FAMILY_JACOBI2D: return L.dtype == PK_DTYPE_I32 ? launch_jacobi2d(L, p, st) : launch_jacobi_wide(L, p, st);
         case PK_FAMILY_MATVEC: return launch_matvec(L, p, st);
         case PK_FAMILY_MATMUL: return launch_matmul(L, p, st);
         case PK_FAMILY_ADDITION: return launch_addition(L, p, st);
@@ -217,12 +217,12 @@ int validate(const pk_launch_t *L, int nptrs) {
     if (L->variant != PK_VARIANT_STAGED && L->variant != PK_VARIANT_DIRECT)
         return fail(PK_E_UNSUPPORTED, "unknown variant %d", L->variant);
     const bool stencil = L->family == PK_FAMILY_JACOBI1D || L->family == PK_FAMILY_JACOBI2D;
-    if (L->dtype < PK_DTYPE_I32 || L->dtype > PK_DTYPE_F64 || (stencil && L->dtype != PK_DTYPE_I32))
+    if (L->dtype < PK_DTYPE_I32 || L->dtype > PK_DTYPE_F64 || (stencil && L->dtype == PK_DTYPE_F32))
         return fail(PK_E_UNSUPPORTED, "dtype %d not provided for family %d", L->dtype, L->family);
     if ((L->flags & PK_FLAG_TF32X3) && !(L->family == PK_FAMILY_MATMUL && L->dtype == PK_DTYPE_F32))
         return fail(PK_E_UNSUPPORTED, "3xTF32 applies to float32 matmul only");
-    if ((L->flags & PK_FLAG_TEMPORAL) && L->family != PK_FAMILY_JACOBI1D && L->family != PK_FAMILY_JACOBI2D)
-        return fail(PK_E_UNSUPPORTED, "temporal blocking is provided for the Jacobi programs only");
+    if ((L->flags & PK_FLAG_TEMPORAL) && !(stencil && L->dtype == PK_DTYPE_I32))
+        return fail(PK_E_UNSUPPORTED, "temporal blocking is provided for the int32 Jacobi programs only");
     return PK_OK;
 }
 
@@ -310,9 +310,21 @@ int pk_launch_checked(const pk_launch_t *L, void *const *dev_ptrs, const int64_t
     return pk_launch(L, dev_ptrs, nptrs, stream);
 }
 
+int pk_launch_block(const pk_launch_t *L, const int64_t *grid, int ngrid, const int64_t *ctx, int nctx,
+                    void *const *dev_ptrs, int nptrs, void *stream) {
+    int rc = validate(L, nptrs);
+    if (rc) return rc;
+    if (ngrid < 0 || ngrid > 2 || nctx < 0 || nctx > 1 || (ngrid && !grid) || (nctx && !ctx))
+        return fail(PK_E_PARAM, "pk_launch_block: %d grid / %d context values", ngrid, nctx);
+    for (int i = 0; i < nptrs; i++)
+        if (!dev_ptrs || !dev_ptrs[i]) return fail(PK_E_PARAM, "array %d is a null pointer", i);
+    return launch_block(*L, grid, ngrid, ctx, nctx, dev_ptrs, static_cast<cudaStream_t>(stream));
+}
+
 int pk_jacobi_sweep(const pk_launch_t *L, const void *src, void *dst, int64_t lo, int64_t hi,
                     void *stream) {
     if (!L || !src || !dst) return fail(PK_E_PARAM, "null argument");
+    if (L->dtype != PK_DTYPE_I32) return fail(PK_E_UNSUPPORTED, "pk_jacobi_sweep: int32 only");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (L->family == PK_FAMILY_JACOBI1D) return sweep_jacobi1d(*L, src, dst, lo, hi, st);
     if (L->family == PK_FAMILY_JACOBI2D) return sweep_jacobi2d(*L, src, dst, lo, hi, st);
@@ -807,7 +819,8 @@ int pk_launch_multi(const pk_launch_t *L, int ndev, const int *devices, void *co
 
     int64_t u0, u1, align;
     const bool stencil = L->family == PK_FAMILY_JACOBI1D || L->family == PK_FAMILY_JACOBI2D;
-    if (ndev == 1 || !covered_units(*L, &u0, &u1, &align)) {  // nothing to split: device 0 runs it
+    // nothing to split (or stencil data the int32 sweeps do not take): device 0 runs it
+    if (ndev == 1 || !covered_units(*L, &u0, &u1, &align) || (stencil && L->dtype != PK_DTYPE_I32)) {
         cudaSetDevice(devices[0]);
         return finish(dispatch(*L, ptrs(0), M.st[0]));
     }

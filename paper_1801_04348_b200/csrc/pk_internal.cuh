@@ -142,6 +142,11 @@ int launch_matmul_kslice(const pk_launch_t &L, void *const *p, int64_t k0, int64
 int launch_matmul_tf32x3(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi,
                          int64_t Nc, int64_t K, cudaStream_t st);
 int launch_addition(const pk_launch_t &L, void *const *p, cudaStream_t st);
+// one thread block of the program (run_block) on any dtype (k_block.cu)
+int launch_block(const pk_launch_t &L, const int64_t *grid, int ngrid, const int64_t *ctx, int nctx, void *const *p,
+                 cudaStream_t st);
+// the Jacobi programs on int64 / binary64 data: per-step sweeps (k_block.cu)
+int launch_jacobi_wide(const pk_launch_t &L, void *const *p, cudaStream_t st);
 
 // Shared-memory words staged per block (0 for direct variants).
 int64_t footprint_words(const pk_launch_t &L);

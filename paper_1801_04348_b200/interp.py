@@ -407,64 +407,160 @@ def _deep_copy(v):
     return v.clone()
 
 
+# grid meta_for variables (outer first) and the serial context loop of each family's program
+GRID_VARS = {"reverse": ("i",), "transpose": ("v0", "v1"), "jacobi": ("i",), "jacobi2d": ("v0", "v1"),
+             "matvec": ("i",), "matmul": ("i", "j"), "addition": ("v0", "v1")}
+CONTEXT_VARS = {"jacobi": ("t",), "jacobi2d": ("t",), "matmul": ("k",)}
+
+
+def _block_accesses(family: str, P: dict, g: tuple, ctx: tuple) -> dict:
+    """Every index one thread block touches, per array and dimension, as
+    (min, max) -- the thread loops and serial loops enumerated exactly (the
+    block's accesses are what interp.py:209-212 bounds-checks).  Empty
+    dict when the thread loops are empty (nothing runs)."""
+    ar = np.arange
+
+    def grid(*ranges):
+        mesh = np.meshgrid(*[ar(r, dtype=np.int64) for r in ranges], indexing="ij")
+        return [m.reshape(-1) for m in mesh]
+
+    def mm(x):
+        return (int(x.min()), int(x.max()))
+
+    N = P["n"] if family == "matmul" else P["N"]
+    s = P.get("s", 1)
+    if family in ("reverse", "jacobi", "matvec"):
+        j, k = grid(max(0, P["B"]), max(0, s))
+        if j.size == 0:
+            return {}
+        p = g[0] * s * P["B"] + k * P["B"] + j
+        if family == "reverse":
+            return {"a": [mm(p)], "c": [mm(N - 1 - p)]}
+        if family == "jacobi":
+            src = N + p if ctx[0] % 2 == 0 else p
+            dst = p + 1 if ctx[0] % 2 == 0 else N + p + 1
+            return {"a": [(min(int(src.min()), int(dst.min())), max(int(src.max()) + 2, int(dst.max())))]}
+        if N <= 0:  # the q loop is empty: the statement never runs
+            return {}
+        return {"a": [mm(p), (0, N - 1)], "x": [(0, N - 1)], "y": [mm(p)]}
+    if family == "matmul":
+        v, u, w = grid(max(0, P["B0"]), max(0, P["ub1"]), max(0, s))
+        if v.size == 0:
+            return {}
+        p = g[0] * P["B0"] + v
+        q = g[1] * P["ub1"] * s + w * P["ub1"] + u
+        out = {"c": [mm(p), mm(q)]}
+        if P["B0"] > 0:
+            kk = (P["B0"] * ctx[0], P["B0"] * ctx[0] + P["B0"] - 1)
+            out["a"] = [mm(p), kk]
+            out["b"] = [kk, mm(q)]
+        return out
+    u0, u1, k = grid(max(0, P["B0"]), max(0, P["B1"]), max(0, s if family != "addition" else 1))
+    if u0.size == 0:
+        return {}
+    if family == "transpose":
+        i = g[0] * P["B0"] + u0
+        jj = (g[1] * s + k) * P["B1"] + u1
+        return {"a": [mm(jj), mm(i)], "c": [mm(i * N + jj)]}
+    if family == "jacobi2d":
+        i = g[0] * P["B0"] + u0 + 1
+        jj = (g[1] * s + k) * P["B1"] + u1 + 1
+        rows = [int(i.min()) - 1, int(i.max()) + 1]
+        if ctx[0] % 2 == 0:
+            return {"a": [(rows[0], N + int(i.max())), (int(jj.min()) - 1, int(jj.max()) + 1)]}
+        return {"a": [(int(i.min()), N + rows[1]), (int(jj.min()) - 1, int(jj.max()) + 1)]}
+    # addition: the guard i < N && j < N/2 (merged: j < N) selects the points that access
+    i = g[0] * P["B0"] + u0
+    jj = g[1] * P["B1"] + u1
+    merged = P.get("_merged", False)
+    keep = (i < N) & (jj < (N if merged else N // 2))
+    if not keep.any():
+        return {}
+    idx = (i * N + jj)[keep]
+    hi = int(idx.max()) + (0 if merged else N // 2)
+    return {n: [(int(idx.min()), hi)] for n in ("a", "b", "c")}
+
+
 def run_block(program, params, grid_values, context_values=None, arrays=None, tracer=None):
     """One thread block (interp.py:228-249): the grid indices fixed to
     ``grid_values``, the serial context loop variables to ``context_values``,
-    the thread loops swept.  Runs the reference emitter's leaf for the
-    program (the original program, or its caching-off case program) with its
-    grid loops pinned, as a single block on the GPU (jit.run_block_leaf).
-    Returns every declared array like run_program; int programs only (the
-    emitted leaves compute on C ints)."""
+    the thread loops swept -- by one CUDA block of the family's block kernel
+    (pk_launch_block, csrc/k_block.cu) in the program's own statement order.
+    Values follow run_program's rules (marshal.py: binary64 for Python
+    floats, int64 where int32 could not hold the values, object words for the
+    permutations); an access outside an array raises ``IndexError`` as the
+    reference does.  Returns every declared array like run_program."""
     global _last
     if tracer is not None:
         raise NotImplementedError(
             "tracer is CPU-only instrumentation of the reference interpreter; "
             "the GPU executor cannot report per-access events"
         )
-    from . import jit
-
     kind = identify(program)
-    if kind.is_original:
-        variant = "original"
-    elif tuple(kind.applied) == ("caching-off",):
-        variant = "caching-off"
-    else:
-        raise NotImplementedError("run_block runs the original program or its caching-off case program, "
-                                  "not %s" % (kind.applied,))
+    rename = dict(kind.rename)
+    grid_values = {rename.get(k, k): v for k, v in dict(grid_values).items()}
+    context_values = {rename.get(k, k): v for k, v in dict(context_values or {}).items()}
+    params = {rename.get(k, k): v for k, v in params.items()}
+    arrays = {rename.get(k, k): v for k, v in dict(arrays or {}).items()}
     fam = FAMILIES[kind.family]
-    arrays = dict(arrays or {})
-    if any(_dtype_of(v) == "f" for n, v in arrays.items() if n in {a.name for a in fam.arrays}):
-        raise NotImplementedError("run_block computes on C ints (the emitted leaves are int kernels)")
+    P = effective_params(kind, params)
+    g = []
+    for name in GRID_VARS[kind.family]:
+        if name not in grid_values:
+            raise KeyError(name)  # the body reads the grid variable (interp.py eval of an unset Name)
+        g.append(int(grid_values[name]))
+    ctx = []
+    for name in CONTEXT_VARS.get(kind.family, ()):
+        if name not in context_values:
+            raise KeyError(name)
+        ctx.append(int(context_values[name]))
     torch = _torch()
     if not torch.cuda.is_available():
         raise RuntimeError("run_block needs a CUDA device (sm_100a); there is no CPU fallback")
-    leaf = jit.packaged_leaf(kind.family, variant)
-    P = effective_params(kind, params)
+    declared = [a.name for a in fam.arrays]
+    plan, srcs = marshal.plan(kind.family, P, {n: arrays[n] for n in declared if n in arrays})
     shapes = _shapes_py(fam, P)
-    kinds = [_kind_of(v) for v in arrays.values()]
-    default_kind = kinds[0] if kinds else "list"
+    merged = kind.family == "addition" and "granularity" in kind.applied
+    acc = _block_accesses(kind.family, dict(P, _merged=merged), tuple(g), tuple(ctx))
+    for name, dims in acc.items():
+        shape = tuple(np.shape(np.asarray(arrays[name], dtype=object))) if name in arrays and \
+            marshal.kind_of(arrays[name]) == "list" else \
+            (tuple(arrays[name].shape) if name in arrays else shapes[name])
+        if len(shape) != len(dims):  # flat data for a 2-D declaration: check the flat extent
+            shape, dims = (int(np.prod(shape)),), [(dims[0][0] * shapes[name][-1] + dims[-1][0],
+                                                    dims[0][1] * shapes[name][-1] + dims[-1][1])]
+        for (lo, hi), n in zip(dims, shape):
+            if lo < 0 or hi >= n:
+                raise IndexError("access %s out of bounds: index %d, size %d" % (name, lo if lo < 0 else hi, n))
     dev = torch.device("cuda", torch.cuda.current_device())
-    bufs, sizes = {}, {}
-    for a in fam.arrays:
-        shape = shapes[a.name]
-        if a.name in arrays:
-            bufs[a.name], sizes[a.name] = _to_device_tensor(a.name, arrays[a.name], shape, np.int32, dev)
+    counts = {n: _numel(shapes[n]) for n in declared}
+    bufs = []
+    for n in declared:
+        if n in srcs:
+            bufs.append(marshal.device_words(plan, srcs[n], counts[n], dev))
+        elif plan.objects:
+            bufs.append(torch.full((max(counts[n], 1),), plan.zero_index, dtype=torch.int64, device=dev))
         else:
-            bufs[a.name] = torch.zeros(max(_numel(shape), 1), dtype=torch.int32, device=dev)
-            sizes[a.name] = _numel(shape)
-    jit.run_block_leaf(leaf, P, dict(grid_values), dict(context_values or {}), bufs,
-                       torch.cuda.current_stream(dev).cuda_stream)
+            bufs.append(torch.zeros(max(counts[n], 1), dtype=marshal.torch_dtype(plan), device=dev))
+    L = binding.make_launch(kind, P, kind.applied, plan.dtype)
+    if acc and all(counts[n] > 0 for n in declared):
+        _lib.launch_block(L, g, ctx, [b.data_ptr() for b in bufs], torch.cuda.current_stream(dev).cuda_stream)
     torch.cuda.current_stream(dev).synchronize()
-    _last = RunInfo(kind.family, None, tuple(kind.applied), False, {"kernel": leaf.kernel_name, "block": True}, 0)
+    _last = RunInfo(kind.family, None, tuple(kind.applied), False,
+                    dict(binding.describe(L), block=True, grid=g, context=ctx), 0)
+    kinds = [marshal.kind_of(v) for v in arrays.values()]
+    default_kind = kinds[0] if kinds else "list"
     out = {}
     for name, v in arrays.items():
-        if name not in bufs:
+        if name not in counts:
             out[name] = _deep_copy(v)
-    for a in fam.arrays:
-        shape = shapes[a.name]
-        like = arrays.get(a.name)
-        k = _kind_of(like) if like is not None else default_kind
-        out[a.name] = _from_device(bufs[a.name][: _numel(shape)], k, shape, like)
+    for n, t in zip(declared, bufs):
+        like = arrays.get(n)
+        k = marshal.kind_of(like) if like is not None else default_kind
+        out[n] = marshal.finish(plan, srcs.get(n), t, shapes[n], k, like)
+    if rename:
+        back = {v: k for k, v in rename.items()}
+        out = {back.get(k, k): v for k, v in out.items()}
     return out
 
 

@@ -22,8 +22,11 @@ result equals the reference's, and refuses (loudly) where it cannot:
   run in int32 when a bound on every result proves int32 holds it (two's
   complement sums are exact modulo 2^32, so the final value is exact), in
   int64 when the bound fits int64, and raise ``OverflowError`` beyond that.
-* **jacobi, jacobi2d**: C ints within int32 (the kernels form exact 64-bit
-  sums where 32 bits could wrap); floats raise ``NotImplementedError``.
+* **jacobi, jacobi2d**: ints within int32 run the int32 register sweeps
+  (exact 64-bit sums where 32 bits could wrap), wider ints int64 sweeps;
+  Python floats / float data run binary64 sweeps whose "/" is the
+  reference's c_div on floats (interp.py:43-46: CPython's float floor
+  division of the absolute values, with the sign) -- bit-identical.
 """
 
 from __future__ import annotations
@@ -198,11 +201,10 @@ def plan(family: str, P: dict, supplied: dict) -> tuple[Plan, dict]:
                         % (bad.name, family))
     floats = vkinds & {"float", "mixed", "f32", "f64"}
     if floats:
-        if family in INT_FAMILIES:
-            raise NotImplementedError("%s computes on C ints; float arrays are not supported" % family)
         # binary64 wherever the reference's Python floats (or float64 data) are
-        # involved; float32 data alone run the float32 path
-        dtype = _lib.DTYPE_F32 if floats == {"f32"} else _lib.DTYPE_F64
+        # involved; float32 data alone run the float32 path -- except for the
+        # stencils, whose "/" is c_div on Python floats (binary64 only)
+        dtype = _lib.DTYPE_F32 if floats == {"f32"} and family not in INT_FAMILIES else _lib.DTYPE_F64
         out = NP_OF_DTYPE[dtype]
         return Plan(family, dtype, out_dtype={n: out for n in srcs}), srcs
     # integers: the narrowest type that provably holds every result
@@ -210,10 +212,16 @@ def plan(family: str, P: dict, supplied: dict) -> tuple[Plan, dict]:
         if s.lo < I64_MIN or s.hi > I64_MAX:
             raise OverflowError("array %s holds values outside int64" % s.name)
     if family in INT_FAMILIES:
-        for s in srcs.values():
-            if s.lo < I32_MIN or s.hi > I32_MAX:
-                raise OverflowError("array %s holds values outside int32" % s.name)
-        return Plan(family, _lib.DTYPE_I32, out_dtype={n: np.dtype(np.int32) for n in srcs}), srcs
+        # an average never leaves its inputs' range: int32 data run the int32
+        # sweeps (64-bit sums where needed); wider data the int64 sweeps, whose
+        # sums of 3 (5) values must fit int64
+        wide = any(s.lo < I32_MIN or s.hi > I32_MAX for s in srcs.values())
+        if wide and 5 * max(_abs_max(s) for s in srcs.values()) > I64_MAX:
+            raise OverflowError("%s: sums of 5 values up to %d leave int64" % (family, max(_abs_max(s) for s in srcs.values())))
+        dt = _lib.DTYPE_I64 if wide else _lib.DTYPE_I32
+        out = {n: np.result_type(NP_OF_DTYPE[dt], s.np_dtype) if s.np_dtype is not None else NP_OF_DTYPE[dt]
+               for n, s in srcs.items()}
+        return Plan(family, dt, out_dtype=out), srcs
     bound = int_bound(family, P, srcs)
     if bound <= I32_MAX:
         dtype = _lib.DTYPE_I32

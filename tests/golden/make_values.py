@@ -23,6 +23,7 @@ and records inputs and outputs.  Only this script touches /root/reference.
 from __future__ import annotations
 
 import argparse
+import itertools
 import json
 import os
 import random
@@ -104,6 +105,76 @@ def main() -> int:
                 want = interp.run_program(prog, dict(params), arrays=seed)
                 vectors.append({"family": family, "params": params, "style": style, "inputs": seed,
                                 "outputs": want})
+    # the stencils on binary64 floats (c_div on Python floats) and on ints
+    # beyond int32, whole programs
+    for family, params in [("jacobi", {"T": 4, "N": 26, "s": 2, "B": 4}), ("jacobi", {"T": 3, "N": 19, "s": 3, "B": 2}),
+                           ("jacobi2d", {"T": 3, "N": 11, "s": 2, "B0": 2, "B1": 2})]:
+        prog = dsl.parse(programs.original(family).text)
+        for style in ("f64", "f64_unit", "i64"):
+            shapes = {}
+            for name, data in interp.Machine(prog, dict(params)).arrays.items():
+                shapes[name] = (len(data), len(data[0])) if data and isinstance(data[0], list) else (len(data),)
+            seed = {name: fill(shape, style, rng) for name, shape in shapes.items()}
+            if style == "i64":  # sums of 5 stay in int64
+                seed = {k: [[x // 8 for x in r] for r in v] if v and isinstance(v[0], list) else [x // 8 for x in v]
+                        for k, v in seed.items()}
+            want = interp.run_program(prog, dict(params), arrays=seed)
+            vectors.append({"family": family, "params": params, "style": style, "inputs": seed, "outputs": want})
+    # run_block (interp.py:228-249) on values beyond 32-bit words: every grid
+    # point of small instances, original programs and their granularity case
+    # programs, binary64 floats and wide ints
+    from parakern import model, strategies  # noqa: E402
+
+    blocks = []
+    BLOCK_PARAMS = {"jacobi": {"T": 3, "N": 26, "s": 2, "B": 4}, "jacobi2d": {"T": 2, "N": 11, "s": 2, "B0": 2, "B1": 2},
+                    "reverse": {"N": 37, "s": 2, "B": 4}, "transpose": {"N": 9, "s": 2, "B0": 2, "B1": 2},
+                    "matvec": {"N": 11, "s": 2, "B": 3}, "matmul": {"n": 8, "B0": 2, "ub1": 2, "s": 2},
+                    "addition": {"N": 8, "B0": 2, "B1": 2}}
+    for family in sorted(BLOCK_PARAMS):
+        a = BLOCK_PARAMS[family]
+        prog = dsl.parse(programs.original(family).text)
+        cfg = model.build_source_cfg(prog)
+        m = interp.Machine(prog, dict(a))
+        grid = [(gv.var, m.eval(gv.bound)) for gv in cfg.grid]
+        context = [(cv.var, m.eval(cv.bound)) for cv in cfg.context]
+        shapes = {}
+        for name, data in m.arrays.items():
+            shapes[name] = (len(data), len(data[0])) if data and isinstance(data[0], list) else (len(data),)
+        for style in ("f64", "i64"):
+            seed = {name: fill(shape, style, rng) for name, shape in shapes.items()}
+            if style == "i64":
+                seed = {k: [[x >> 40 for x in r] for r in v] if v and isinstance(v[0], list) else [x >> 40 for x in v]
+                        for k, v in seed.items()}  # |v| < 2^22: products and sums stay in int64
+            ctx = {v: rng.randrange(max(1, b)) for v, b in context}
+            for point in itertools.product(*[range(b) for _, b in grid]):
+                gv = {v: p for (v, _), p in zip(grid, point)}
+                want = interp.run_block(prog, dict(a), gv, dict(ctx), arrays=seed)
+                blocks.append({"family": family, "style": style, "program": "original", "params": a,
+                               "grid_values": gv, "context_values": ctx, "inputs": seed, "outputs": want})
+            # one grid point past the meta_for range: the reference raises IndexError
+            gv = {v: b for v, b in grid}
+            try:
+                interp.run_block(prog, dict(a), gv, dict(ctx), arrays=seed)
+                err = None
+            except IndexError:
+                err = "IndexError"
+            blocks.append({"family": family, "style": style, "program": "original", "params": a, "grid_values": gv,
+                           "context_values": ctx, "inputs": seed, "error": err})
+        # the granularity case program (s removed, s := 1), one grid point
+        try:
+            gp = strategies.apply_source("granularity", prog)
+        except ValueError:
+            continue
+        ga = {k: v for k, v in a.items() if k != "s"}
+        gm = interp.Machine(gp, dict(ga))
+        gcfg = model.build_source_cfg(gp)
+        ggrid = {gv.var: 0 for gv in gcfg.grid}
+        gctx = {cv.var: 0 for cv in gcfg.context}
+        gshapes = {n: ((len(d), len(d[0])) if d and isinstance(d[0], list) else (len(d),)) for n, d in gm.arrays.items()}
+        seed = {name: fill(shape, "f64", rng) for name, shape in gshapes.items()}
+        want = interp.run_block(gp, dict(ga), ggrid, dict(gctx), arrays=seed)
+        blocks.append({"family": family, "style": "f64", "program": dsl.render(gp), "params": ga,
+                       "grid_values": ggrid, "context_values": gctx, "inputs": seed, "outputs": want})
     # IndexError (interp.py:209-212): the shortest 1-D array each program runs
     # on without an out-of-bounds access -- what pk_required_elems must report
     bounds = []
@@ -130,7 +201,8 @@ def main() -> int:
     out = os.path.join(HERE, "value_vectors.json")
     with open(out, "w") as fh:
         json.dump({"generator": "parakern.interp.run_program via tests/golden/make_values.py",
-                   "seed": "0x64F", "vectors": vectors, "bounds": bounds}, fh, separators=(",", ":"))
+                   "seed": "0x64F", "vectors": vectors, "bounds": bounds, "blocks": blocks}, fh,
+                  separators=(",", ":"))
         fh.write("\n")
     print("wrote", out, len(vectors), "vectors", os.path.getsize(out), "bytes")
     return 0

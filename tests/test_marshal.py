@@ -42,10 +42,12 @@ def test_arith_plans_pick_exact_types():
     assert marshal.plan("matvec", P, {"a": np.ones((4, 4), np.float32), "x": np.ones(4)})[0].dtype == _lib.DTYPE_F64
     with pytest.raises(TypeError):
         marshal.plan("matvec", P, {"a": [["x"] * 4] * 4})
-    with pytest.raises(NotImplementedError):
-        marshal.plan("jacobi", {"T": 1, "N": 6, "s": 1, "B": 2}, {"a": [0.5] * 12})
+    J = {"T": 1, "N": 6, "s": 1, "B": 2}
+    assert marshal.plan("jacobi", J, {"a": [0.5] * 12})[0].dtype == _lib.DTYPE_F64  # c_div on Python floats
+    assert marshal.plan("jacobi", J, {"a": np.ones(12, np.float32)})[0].dtype == _lib.DTYPE_F64
+    assert marshal.plan("jacobi", J, {"a": [2**31] * 12})[0].dtype == _lib.DTYPE_I64
     with pytest.raises(OverflowError):
-        marshal.plan("jacobi", {"T": 1, "N": 6, "s": 1, "B": 2}, {"a": [2**31] * 12})
+        marshal.plan("jacobi", J, {"a": [2**62] * 12})
 
 
 def test_int_bound_is_an_upper_bound_on_the_reference_results():
