@@ -246,6 +246,70 @@ int launch_tiled(const T *a, const T *b, T *c, int64_t n, int64_t K, int64_t rlo
     return after_launch("matmul_tiled");
 }
 
+// binary64 / int64: the same c + a*b sequence (two roundings per step for
+// binary64, wrapping int64) on a 64 x 64 tile of 256 threads, each owning
+// rows ty + 16i and columns tx + 16j (i, j < 4) so the a reads of a warp are
+// 2-address broadcasts and the b reads 128-byte rows; 16-deep k slabs of a
+// (row-major, pitch 18) and b double-buffered by cp.async.
+constexpr int kXM = 64, kXN = 64, kXK = 16, kXAP = kXK + 2;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_matmul_exact_tiled(const T *__restrict__ a, const T *__restrict__ b,
+                                                           T *__restrict__ c, int64_t n, int64_t K, int64_t rlo,
+                                                           int64_t ntn) {
+    __shared__ __align__(16) T As[2][kXM][kXAP];
+    __shared__ __align__(16) T Bs[2][kXK][kXN];
+    constexpr int V = 16 / sizeof(T);
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    const int64_t bid = blockIdx.x;
+    const int64_t m0 = rlo + (bid / ntn) * kXM, n0 = (bid % ntn) * kXN;
+    auto load = [&](int64_t k0, int buf) {
+        for (int e = tid; e < kXM * (kXK / V); e += 256) {
+            const int r = e / (kXK / V), cv = e % (kXK / V);
+            cp_async16(&As[buf][r][cv * V], a + (m0 + r) * n + k0 + cv * V, 16);
+        }
+        for (int e = tid; e < kXK * (kXN / V); e += 256) {
+            const int r = e / (kXN / V), cv = e % (kXN / V);
+            cp_async16(&Bs[buf][r][cv * V], b + (k0 + r) * n + n0 + cv * V, 16);
+        }
+        cp_async_commit();
+    };
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = c[(m0 + ty + 16 * i) * n + n0 + tx + 16 * j];
+    const int64_t nk = K / kXK;
+    load(0, 0);
+    for (int64_t kt = 0; kt < nk; kt++) {
+        if (kt + 1 < nk) {
+            load((kt + 1) * kXK, (int)((kt + 1) & 1));
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int buf = (int)(kt & 1);
+#pragma unroll
+        for (int kk = 0; kk < kXK; kk++) {
+            T av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) av[i] = As[buf][ty + 16 * i][kk];
+#pragma unroll
+            for (int j = 0; j < 4; j++) bv[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = mad(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) c[(m0 + ty + 16 * i) * n + n0 + tx + 16 * j] = acc[i][j];
+}
+
 template <typename T>
 int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo, int64_t rhi,
              int64_t Nc, int64_t K) {
@@ -270,6 +334,16 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
             if (BM == 64 && BN == 128) return launch_tiled<T, 8, 16, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
             if (BM == 128 && BN == 64) return launch_tiled<T, 16, 8, 8>(a, b, c, L.N, K, rlo, rhi, Nc, st);
             if (BM == 64 && BN == 64) return launch_tiled<T, 8, 8, 16>(a, b, c, L.N, K, rlo, rhi, Nc, st);
+        }
+    }
+    if constexpr (sizeof(T) == 8) {
+        if (!generic && (rhi - rlo) % kXM == 0 && Nc % kXN == 0 && K % kXK == 0 && L.N % 2 == 0 &&
+            aligned16(a) && aligned16(b) && aligned16(c)) {
+            const int64_t ntn = Nc / kXN, blocks = (rhi - rlo) / kXM * ntn;
+            if (blocks <= 0) return PK_OK;
+            if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matmul: grid too large");
+            k_matmul_exact_tiled<T><<<(unsigned)blocks, 256, 0, st>>>(a, b, c, L.N, K, rlo, ntn);
+            return after_launch("matmul_exact_tiled");
         }
     }
     if (L.B0 * L.ub1 > 1024)

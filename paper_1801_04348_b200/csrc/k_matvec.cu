@@ -324,8 +324,81 @@ __global__ void __launch_bounds__(kExactRows) k_matvec_exact(const T *__restrict
     if (live) y[r0 + t] = acc;
 }
 
+// The same sequence fed by cp.async: a block owns groups of kXR = 16 rows
+// (one computing thread per row, every thread loading), 256-column stages
+// of a (32 KB) double-buffered in shared memory, the next stage in flight
+// while the 16 chains run over the current one; persistent blocks stride
+// over the row groups (32768 rows: 2048 groups on 3 x 148 blocks).  Needs
+// N even and 16-byte aligned operands (rows then start on 16 bytes).
+constexpr int kXR = 32, kXC = 128, kXT = 128, kXPitch = kXC + 2;  // pitch: 16-byte rows, 2-way banks
+
+template <typename T>
+__global__ void __launch_bounds__(kXT) k_matvec_exact_async(const T *__restrict__ a, const T *__restrict__ x,
+                                                           T *__restrict__ y, int64_t N, int64_t rlo, int64_t rhi) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *tile = reinterpret_cast<T *>(smem_raw);  // [2][kXR][kXPitch]
+    T *xs = tile + 2 * kXR * kXPitch;           // [2][kXC]
+    const int t = threadIdx.x;
+    const int64_t ngroups = ceil_div(rhi - rlo, kXR), nchunks = ceil_div(N, kXC);
+    constexpr int V = 16 / sizeof(T);            // elements per 16-byte copy
+    auto load = [&](int64_t r0, int64_t c, int buf) {
+        const int64_t q0 = c * kXC;
+        T *tb = tile + buf * kXR * kXPitch;
+        for (int e = t; e < kXR * (kXC / V); e += kXT) {
+            const int rr = e / (kXC / V), cv = e % (kXC / V);
+            const int64_t row = r0 + rr, q = q0 + (int64_t)cv * V;
+            const bool ok = row < rhi && q < N;
+            cp_async16(tb + rr * kXPitch + cv * V, ok ? (const void *)(a + row * N + q) : (const void *)a,
+                       ok ? 16 : 0);
+        }
+        for (int e = t; e < kXC / V; e += kXT) {
+            const int64_t q = q0 + (int64_t)e * V;
+            cp_async16(xs + buf * kXC + e * V, q < N ? (const void *)(x + q) : (const void *)x, q < N ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+    for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int64_t r0 = rlo + g * kXR;
+        const bool live = t < kXR && r0 + t < rhi;
+        T acc = live ? y[r0 + t] : T(0);
+        load(r0, 0, 0);
+        for (int64_t c = 0; c < nchunks; c++) {
+            if (c + 1 < nchunks) {
+                load(r0, c + 1, (int)((c + 1) & 1));
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            if (live) {
+                const T *row = tile + (c & 1) * kXR * kXPitch + t * kXPitch;
+                const T *xc = xs + (c & 1) * kXC;
+                const int nc = (int)min((int64_t)kXC, N - c * kXC);
+                for (int cc = 0; cc < nc; cc++) acc = madd(acc, row[cc], xc[cc]);
+            }
+            __syncthreads();  // the buffer is refilled two stages on
+        }
+        if (live) y[r0 + t] = acc;
+    }
+}
+
 template <typename T>
 int launch_exact(void *const *p, int64_t N, int64_t rlo, int64_t rhi, cudaStream_t st) {
+    if (N % 2 == 0 && aligned16(p[0]) && aligned16(p[1])) {
+        const size_t smem = (size_t)(2 * kXR * kXPitch + 2 * kXC) * sizeof(T);
+        int rc = allow_smem((const void *)k_matvec_exact_async<T>, smem);
+        if (rc) return rc;
+        int dev = 0, sms = 148, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matvec_exact_async<T>, kXT, smem);
+        int64_t blocks = ceil_div(rhi - rlo, kXR);
+        const int64_t slots = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+        if (blocks > slots) blocks = slots;
+        k_matvec_exact_async<T><<<(unsigned)blocks, kXT, smem, st>>>(
+            static_cast<const T *>(p[0]), static_cast<const T *>(p[1]), static_cast<T *>(p[2]), N, rlo, rhi);
+        return after_launch("matvec_exact_async");
+    }
     const int64_t blocks = ceil_div(rhi - rlo, kExactRows);
     if (blocks > 0x7fffffffLL) return fail(PK_E_UNSUPPORTED, "matvec: grid too large");
     k_matvec_exact<T><<<(unsigned)blocks, kExactRows, 0, st>>>(static_cast<const T *>(p[0]),

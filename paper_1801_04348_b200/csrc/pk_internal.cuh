@@ -32,7 +32,7 @@ cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t max0(int64_t v) { return v > 0 ? v : 0; }
 
 // --- device helpers ----------------------------------------------------------
@@ -94,6 +94,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+
+// Asynchronous 16-byte global -> shared copy (cp.async.cg); bytes < 16
+// zero-fills the rest of the destination (0: a pure zero fill).
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Truncating integer division of an exact (64-bit) sum, as the reference's
 // c_div (interp.py:43-46): C division already truncates toward zero.

@@ -28,6 +28,10 @@ def main():
     mv = machine_mod.live()
     sel = cases.select(kind, params, mv)
     dtype = _lib.DTYPE_F32 if fam == "matmul" or "--f32" in sys.argv else _lib.DTYPE_I32
+    if "--f64" in sys.argv:
+        dtype = _lib.DTYPE_F64
+        mv = machine_mod.live(elem_bytes=8)
+        sel = cases.select(kind, params, mv)
     L = binding.make_launch(kind, params, sel.applied, dtype, generic=generic, extra_flags=extra)
     if temporal:
         L.tblock = temporal[0]
@@ -39,6 +43,8 @@ def main():
             n *= d
         if dtype == _lib.DTYPE_F32:
             bufs.append(torch.rand(n, device="cuda") - 0.5)
+        elif dtype == _lib.DTYPE_F64:
+            bufs.append(torch.rand(n, device="cuda", dtype=torch.float64) - 0.5)
         else:
             bufs.append(torch.randint(-1000, 1000, (n,), dtype=torch.int32, device="cuda"))
     st = torch.cuda.current_stream().cuda_stream
