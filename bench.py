@@ -37,7 +37,17 @@ MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 NCU_TRAFFIC = os.path.join(REPO, "profiles", "ncu_traffic.json")
 # which committed ncu capture describes each measured kernel (tools/make_profiles.py)
 TRAFFIC_KEYS = {"matmul": "matmul_n8192", "reverse": "reverse_2p30", "transpose": "transpose_32768",
-                "jacobi": "jacobi1d_2p28", "jacobi2d": "jacobi2d_16384", "matvec": "matvec_32768"}
+                "jacobi": "jacobi1d_2p28", "jacobi2d": "jacobi2d_16384", "matvec": "matvec_32768",
+                "matvec_f32": "matvec_f32_32768", "addition": "addition_16384", "matmul_n2048": "matmul_n2048"}
+
+
+def traffic_entry(key: str, algorithmic: float):
+    """The committed ncu capture's DRAM bytes per launch beside the algorithmic bytes."""
+    rec = ncu_traffic(TRAFFIC_KEYS[key])
+    if rec is None:
+        return None
+    return {"dram_bytes": rec["bytes"], "algorithmic_bytes": algorithmic, "ratio": round(rec["bytes"] / algorithmic, 4),
+            "kernel": rec["kernel"], "source": rec["report"]}
 
 
 def ncu_traffic(key: str):
@@ -738,6 +748,7 @@ def bench_kernels(peaks, mv, no_tune: bool = False, cpu: bool = True) -> dict:
                              "value": round(gbs, 1), "unit": "GB/s",
                              "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
                              "parity": "within 2 fp32 ulps of binary64" if ok else "MISMATCH",
+                             "traffic": traffic_entry("matvec_f32", 4 * Nm * Nm + 8 * Nm),
                              "note": "float32 a, x, y; products split exactly and summed as a double-float pair"}
         del bufs, want
         torch.cuda.empty_cache()
@@ -776,7 +787,7 @@ def bench_addition(peaks, mv, threads: int) -> dict:
     torch.cuda.empty_cache()
     rec = {"params": P, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 3), "value": round(gbs, 1),
            "unit": "GB/s", "frac_of_measured_hbm": round(gbs / peaks["hbm_gbs"], 4),
-           "parity": parity_check("addition", P, L, gen)}
+           "parity": parity_check("addition", P, L, gen), "traffic": traffic_entry("addition", work)}
     if threads:
         rec["cpu_baseline"] = cpu_sample("addition", threads)
     return rec
@@ -819,7 +830,8 @@ def bench_matmul_n2048(peaks, mv, no_tune: bool, threads: int) -> dict:
     err = matmul_error(L, bufs, n2, 0, n2)
     rec = {"params": tuned, "case": sel.index, "applied": list(sel.applied), "ms": round(ms, 4),
            "value": round(gf, 1), "unit": "GFLOP/s", "frac_of_fp32_peak": round(gf / peak, 4),
-           "tuning_trials": len(trials), "parity": parity_text(err, n2)}
+           "tuning_trials": len(trials), "parity": parity_text(err, n2),
+           "traffic": traffic_entry("matmul_n2048", 4.0 * n2 * n2 * 4) if tuned == base else None}
     del bufs
     torch.cuda.empty_cache()
     if threads:
