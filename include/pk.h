@@ -159,6 +159,18 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
  * what the run touches or copies (the declared extent of each array). */
 int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device);
 
+/* The host-buffer run with separate inputs and outputs: array i is read from
+ * in_ptrs[i] (NULL: zeros) and its final contents are written to
+ * out_ptrs[i] (NULL: not copied back; may equal in_ptrs[i]) -- the result
+ * for an array the program writes, a copy of the input for one it does not
+ * (the reference's deep copy, made in the same pass that stages the input)
+ * -- so a caller's buffers need not be copied to keep them unmutated.  Pinned buffers
+ * move by DMA directly; pageable ones are staged inside the pipeline through
+ * a pinned ring (host copies by a thread pool, overlapped with the DMA and
+ * the kernels).  elems[i] counts both buffers of array i (PK_E_BOUNDS). */
+int pk_run_host_io(const pk_launch_t *L, const void *const *in_ptrs, void *const *out_ptrs, const int64_t *elems,
+                   int nptrs, int device);
+
 /* One thread block of the program (the reference's run_block,
  * interp.py:228-249): grid[0..ngrid) the grid meta_for indices (outer
  * first: reverse / jacobi / matvec i; transpose / jacobi2d / addition

@@ -59,6 +59,7 @@ EXPORTS = (
     "pk_required_elems",
     "pk_run_host",
     "pk_run_host_checked",
+    "pk_run_host_io",
     "pk_launch_multi",
     "pk_jacobi_sweep",
     "pk_launch_block",
@@ -174,6 +175,9 @@ def load() -> ctypes.CDLL:
         lib.pk_run_host_checked.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), i64p, ctypes.c_int,
                                             ctypes.c_int]
         lib.pk_run_host_checked.restype = ctypes.c_int
+        lib.pk_run_host_io.argtypes = [ctypes.POINTER(PkLaunch), ctypes.POINTER(vp), ctypes.POINTER(vp), i64p,
+                                       ctypes.c_int, ctypes.c_int]
+        lib.pk_run_host_io.restype = ctypes.c_int
         lib.pk_launch_multi.argtypes = [ctypes.POINTER(PkLaunch), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int64, ctypes.c_int]
         lib.pk_launch_multi.restype = ctypes.c_int
@@ -260,6 +264,13 @@ def run_host(L: PkLaunch, host_ptrs, device: int = 0, elems=None) -> None:
     else:
         n = (ctypes.c_int64 * len(elems))(*[int(e) for e in elems])
         check(lib.pk_run_host_checked(ctypes.byref(L), arr, n, len(host_ptrs), device))
+
+
+def run_host_io(L: PkLaunch, in_ptrs, out_ptrs, elems, device: int = 0) -> None:
+    """pk_run_host_io: inputs and outputs in separate host buffers (None / 0 = absent)."""
+    n = (ctypes.c_int64 * len(elems))(*[int(e) for e in elems])
+    check(load().pk_run_host_io(ctypes.byref(L), ptr_array([p or 0 for p in in_ptrs]),
+                                ptr_array([p or 0 for p in out_ptrs]), n, len(in_ptrs), device))
 
 
 def launch_checked(L: PkLaunch, ptrs, elems, stream: int = 0) -> None:

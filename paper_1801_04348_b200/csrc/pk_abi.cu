@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <vector>
 
 #include "pk_internal.cuh"
@@ -479,7 +480,12 @@ void host_run_release(HostRun &R, bool healthy) {
 
 }  // namespace
 
-int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device) {
+namespace {
+int run_host_io(const pk_launch_t *L, const void *const *in_ptrs, void *const *out_ptrs, int nptrs, int device);
+}
+
+int pk_run_host_io(const pk_launch_t *L, const void *const *in_ptrs, void *const *out_ptrs, const int64_t *elems,
+                   int nptrs, int device) {
     int rc = validate(L, nptrs);
     if (rc) return rc;
     if (!elems) return fail(PK_E_PARAM, "null element counts");
@@ -489,20 +495,38 @@ int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int6
     ArraySpec spec;
     array_spec(*L, &spec);
     for (int i = 0; i < nptrs; i++) {
-        // pk_run_host moves the declared extent of every array it is given
-        const int64_t want = host_ptrs && host_ptrs[i] ? spec.elems[i] : 0;
+        // the run moves the declared extent of every array it is given
+        const bool given = (in_ptrs && in_ptrs[i]) || (out_ptrs && out_ptrs[i]);
+        const int64_t want = given ? spec.elems[i] : 0;
         if (elems[i] < need[i] || elems[i] < want)
             return fail(PK_E_BOUNDS, "array %d: %lld elements, the run touches %lld and copies %lld", i,
                         (long long)elems[i], (long long)need[i], (long long)want);
     }
-    return pk_run_host(L, host_ptrs, nptrs, device);
+    return run_host_io(L, in_ptrs, out_ptrs, nptrs, device);
+}
+
+int pk_run_host_checked(const pk_launch_t *L, void *const *host_ptrs, const int64_t *elems, int nptrs, int device) {
+    return pk_run_host_io(L, reinterpret_cast<const void *const *>(host_ptrs), host_ptrs, elems, nptrs, device);
 }
 
 int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int device) {
     int rc = validate(L, nptrs);
     if (rc) return rc;
+    return run_host_io(L, reinterpret_cast<const void *const *>(host_ptrs), host_ptrs, nptrs, device);
+}
+
+namespace {
+
+int run_host_io(const pk_launch_t *L, const void *const *in_ptrs, void *const *out_ptrs, int nptrs, int device) {
+    int rc = PK_OK;
     ArraySpec spec;
     array_spec(*L, &spec);
+    const void *in[3] = {nullptr, nullptr, nullptr};
+    void *out[3] = {nullptr, nullptr, nullptr};
+    for (int i = 0; i < nptrs && i < 3; i++) {
+        in[i] = in_ptrs ? in_ptrs[i] : nullptr;
+        out[i] = out_ptrs ? out_ptrs[i] : nullptr;
+    }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(PK_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
 
@@ -574,14 +598,43 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
                 slice = 0;
         if (slice < 0) slice = 0;
     }
+    // Pageable buffers are staged inside the pipeline (pk_staging.cu): their
+    // host copies overlap the DMA and the kernels instead of preceding them
+    bool in_pg[3] = {false, false, false}, out_pg[3] = {false, false, false};
+    size_t out_off[3] = {0, 0, 0}, out_total = 0;
+    for (int i = 0; i < spec.count; i++) {
+        in_pg[i] = in[i] && !host_is_pinned(in[i]);
+        out_pg[i] = spec.written[i] && out[i] && !host_is_pinned(out[i]);
+        if (out_pg[i]) {
+            out_off[i] = out_total;
+            out_total += (size_t)spec.elems[i] * eb;
+        }
+    }
+    StageSession *stage = nullptr;
+    alignas(StageSession) unsigned char stage_mem[sizeof(StageSession)];
+    if (rc == PK_OK && (in_pg[0] || in_pg[1] || in_pg[2] || out_total)) {
+        stage = new (stage_mem) StageSession(device);
+        if (out_total) rc = stage->reserve_out(out_total);
+    }
+    // an array the program never writes, given an output buffer, ends there as
+    // a copy of its input (the reference's deep copy, interp.py:183-186): made
+    // in the same pass that stages the input, or right after its DMA is issued
+    auto copy_out = [&](int i, int64_t off) -> char * {
+        return (!spec.written[i] && out[i] && out[i] != in[i]) ? static_cast<char *>(out[i]) + off * eb : nullptr;
+    };
     auto up_range = [&](int i, int64_t off, int64_t cnt) -> int {
         char *d = static_cast<char *>(R.dev[i]) + off * eb;
-        if (cnt && host_ptrs[i]) {
-            cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(host_ptrs[i]) + off * eb, (size_t)cnt * eb,
+        char *keep = copy_out(i, off);
+        if (cnt && in[i] && in_pg[i]) {
+            return stage->h2d(d, static_cast<const char *>(in[i]) + off * eb, (size_t)cnt * eb, R.h2d, keep);
+        } else if (cnt && in[i]) {
+            cudaError_t x = cudaMemcpyAsync(d, static_cast<const char *>(in[i]) + off * eb, (size_t)cnt * eb,
                                             cudaMemcpyHostToDevice, R.h2d);
             if (x != cudaSuccess) return fail(PK_E_CUDA, "H2D copy: %s", cudaGetErrorString(x));
+            if (keep) parallel_copy(keep, static_cast<const char *>(in[i]) + off * eb, (size_t)cnt * eb);
         } else if (cnt) {
             cudaMemsetAsync(d, 0, (size_t)cnt * eb, R.h2d);  // missing arrays are zero-filled (interp.py:79-81)
+            if (keep) memset(keep, 0, (size_t)cnt * eb);
         }
         return PK_OK;
     };
@@ -593,8 +646,11 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     auto down = [&](const pk_launch_t &C, int i) -> int {
         int64_t off, cnt;
         array_range(C, i, spec.elems[i], &off, &cnt);
-        if (!spec.written[i] || !cnt || !host_ptrs[i]) return PK_OK;
-        cudaError_t x = cudaMemcpyAsync(static_cast<char *>(host_ptrs[i]) + off * eb,
+        if (!spec.written[i] || !cnt || !out[i]) return PK_OK;
+        if (out_pg[i])
+            return stage->d2h(static_cast<char *>(out[i]) + off * eb, out_off[i] + (size_t)off * eb,
+                              static_cast<char *>(R.dev[i]) + off * eb, (size_t)cnt * eb, R.d2h);
+        cudaError_t x = cudaMemcpyAsync(static_cast<char *>(out[i]) + off * eb,
                                         static_cast<char *>(R.dev[i]) + off * eb, (size_t)cnt * eb,
                                         cudaMemcpyDeviceToHost, R.d2h);
         return x == cudaSuccess ? PK_OK : fail(PK_E_CUDA, "D2H copy: %s", cudaGetErrorString(x));
@@ -674,6 +730,10 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
     // the chunked families writes one; kept for completeness)
     for (int i = 0; i < spec.count && rc == PK_OK; i++)
         if (whole[i] && nchunks > 1) rc = down(*L, i);
+    if (stage) {  // copy the staged downloads out as their pieces land, then release the staging
+        const int drc = stage->drain();
+        if (rc == PK_OK) rc = drc;
+    }
     cudaError_t se = cudaSuccess;
     for (cudaStream_t s : R.cs) {
         if (!s) continue;
@@ -698,8 +758,12 @@ int pk_run_host(const pk_launch_t *L, void *const *host_ptrs, int nptrs, int dev
         if (R.dev[i]) cudaFreeAsync(R.dev[i], R.d2h);
     cudaError_t fe = R.d2h ? cudaStreamSynchronize(R.d2h) : cudaSuccess;
     host_run_release(R, se == cudaSuccess && fe == cudaSuccess && e == cudaSuccess);
+    if (stage) stage->~StageSession();
     return rc;
 }
+
+}  // namespace
+
 
 // ---------------------------------------------------------------------------
 // Single-process multi-GPU.

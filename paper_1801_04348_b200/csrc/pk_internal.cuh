@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 
 #include "pk.h"
 
@@ -21,6 +22,33 @@ inline int after_launch(const char *what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return PK_OK;
 }
+
+// Pageable host buffers inside pk_run_host_io (pk_staging.cu).
+bool host_is_pinned(const void *p);
+void parallel_copy(void *dst, const void *src, size_t bytes);  // host memcpy on the staging thread pool
+class StageSession {
+  public:
+    explicit StageSession(int device);
+    ~StageSession();
+    // src (pageable) -> dst (device) through the pinned ring, DMA on st; with
+    // copy_dst, the same pass also copies src there (the caller's result copy)
+    int h2d(void *dst, const void *src, size_t bytes, cudaStream_t st, void *copy_dst = nullptr);
+    // device src -> pinned staging at stage_off (reserve_out first) on st;
+    // copied on to dst (pageable) by drain()
+    int reserve_out(size_t bytes);
+    int d2h(void *dst, size_t stage_off, const void *src, size_t bytes, cudaStream_t st);
+    int drain();
+
+  private:
+    struct Drain {
+        cudaEvent_t ev;
+        const char *stage;
+        char *dst;
+        size_t bytes;
+    };
+    int device_;
+    std::vector<Drain> drains_;
+};
 
 // Opt a kernel into more than 48 KB of dynamic shared memory.
 int allow_smem(const void *kernel, size_t bytes);

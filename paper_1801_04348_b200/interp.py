@@ -311,23 +311,43 @@ def run_program(
     words, out, owned = {}, {}, False
     written = set(fam.written)
     if not on_device and not multi and not inplace:
-        # host arrays: pinned staging + pk_run_host (its PCIe copies overlap the
-        # kernels); while the GPU runs, this thread copies out the arrays the
-        # program never writes (the reference deep-copies them, interp.py:183-186)
+        # host arrays: pk_run_host_io reads the caller's own buffers where they
+        # already hold the plan's words (pageable memory is staged inside the
+        # pipeline, overlapped with the DMA and the kernels) and writes results
+        # into fresh arrays; other inputs are converted into pooled pinned
+        # buffers.  While the GPU runs, this thread copies out the arrays the
+        # program never writes (the reference deep-copies them, interp.py:183-186).
         owned = True
+        copied = {}
         with _pinned.lock:
-            bufs = []
+            ins, outs = [], []
             for i, n in enumerate(declared):
-                buf = _pinned.view(i, counts[n], plan.np_dtype)
-                marshal.host_words(plan, srcs.get(n), counts[n], buf)
-                bufs.append(buf)
+                src = srcs.get(n)
+                direct = marshal.direct_words(plan, src, counts[n])
+                if direct is not None:
+                    ins.append(direct.ctypes.data)
+                    keep = direct  # noqa: F841 -- alive until the call returns
+                elif src is None and not plan.objects:
+                    ins.append(0)  # zeros (interp.py:79-81)
+                else:
+                    buf = _pinned.view(i, counts[n], plan.np_dtype)
+                    marshal.host_words(plan, src, counts[n], buf)
+                    ins.append(buf.ctypes.data)
+                if n in written:
+                    words[n] = marshal.fresh_array(counts[n], plan.np_dtype)
+                    outs.append(words[n].ctypes.data)
+                elif direct is not None and direct.size == counts[n] > 0 and runnable:
+                    # the library copies the input into a fresh array in the pass that stages it
+                    copied[n] = marshal.fresh_array(counts[n], direct.dtype)
+                    outs.append(copied[n].ctypes.data)
+                else:
+                    outs.append(0)
             failure = []
             worker = None
             if runnable:
                 def work():
                     try:
-                        _lib.run_host(L, [b.ctypes.data for b in bufs], dev.index,
-                                      elems=[counts[n] for n in declared])
+                        _lib.run_host_io(L, ins, outs, [counts[n] for n in declared], dev.index)
                     except BaseException as exc:  # re-raised on the caller's thread
                         failure.append(exc)
 
@@ -335,7 +355,7 @@ def run_program(
                 worker.start()
             try:
                 for n in declared:
-                    if n not in written:
+                    if n not in written and n not in copied:
                         like = arrays.get(n)
                         k = marshal.kind_of(like) if like is not None else default_kind
                         out[n] = marshal.copy_input(plan, srcs.get(n), shapes[n], k, like)
@@ -344,9 +364,20 @@ def run_program(
                     worker.join()
             if failure:
                 raise failure[0]
-            for n, buf in zip(declared, bufs):
-                if n in written:
-                    words[n] = marshal.fresh_copy(buf[: counts[n]])
+            for n, arr in copied.items():
+                src = srcs[n]
+                like = arrays.get(n)
+                k = marshal.kind_of(like)
+                arr = arr.view(src.value.dtype) if k == "numpy" else arr
+                out[n] = marshal.finish_copy(arr, src, shapes[n], k, like)
+            if not runnable:  # nothing ran: the written arrays hold their inputs
+                for i, n in enumerate(declared):
+                    if n in written:
+                        src = srcs.get(n)
+                        if src is None and not plan.objects:
+                            words[n][:] = 0
+                        else:
+                            marshal.host_words(plan, src, counts[n], words[n])
     else:
         stream = torch.cuda.current_stream(dev).cuda_stream
         with torch.cuda.device(dev):

@@ -30,3 +30,17 @@ for i in range(4):
     _lib.run_host(L, [x.data_ptr() for x in h], 0)
     dt = time.perf_counter() - t0
     print("pk_run_host pinned %.2f ms  %.1f TFLOP/s" % (dt * 1e3, 2 * n**3 / dt / 1e12), flush=True)
+# the native host path alone: pageable numpy in, fresh numpy out (pk_run_host_io)
+out = np.empty((n, n), np.float32)
+for i in range(4):
+    t0 = time.perf_counter()
+    _lib.run_host_io(L, [a.ctypes.data, b.ctypes.data, c.ctypes.data], [0, 0, out.ctypes.data], [n * n] * 3, 0)
+    dt = time.perf_counter() - t0
+    print("pk_run_host_io pageable %.2f ms  %.1f TFLOP/s" % (dt * 1e3, 2 * n**3 / dt / 1e12), flush=True)
+import torch as _t  # noqa: E402
+for i in range(3):
+    t0 = time.perf_counter()
+    x = _t.from_numpy(a).clone()
+    y = _t.from_numpy(b).clone()
+    dt = time.perf_counter() - t0
+    print("clone a, b (512 MB) %.2f ms" % (dt * 1e3), flush=True)
