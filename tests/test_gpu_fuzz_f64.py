@@ -118,3 +118,57 @@ def test_random_binary64_bit_exact(cuda, family):
             nan = np.isnan(w)
             assert np.array_equal(np.isnan(g), nan), (family, P, k)
             assert np.array_equal(g[~nan].view(np.uint64), w[~nan].view(np.uint64)), (family, P, k)
+
+
+def _restate_int(family, P, arr):
+    """The programs on Python-int semantics for values whose results stay in
+    int64 (numpy int64 arithmetic is then exact); Jacobi divides by C
+    truncation (interp.py:43-46 on ints)."""
+    out = {k: v.copy() for k, v in arr.items()}
+    if family == "addition":
+        N = P["N"]
+        I, J, h = (N // P["B0"]) * P["B0"], min((N // (2 * P["B1"])) * P["B1"], N // 2), N // 2
+        a, b, c = (x.reshape(N, N) for x in (arr["a"], arr["b"], out["c"]))
+        c[:I, :J] = a[:I, :J] + b[:I, :J]
+        c[:I, h:h + J] = a[:I, h:h + J] + b[:I, h:h + J]
+    elif family == "matvec":
+        N, t = P["N"], P["s"] * P["B"]
+        R = (N // t) * t
+        out["y"][:R] = arr["y"][:R] + arr["a"][:R] @ arr["x"]
+    elif family == "matmul":
+        n = P["n"]
+        M = K = (n // P["B0"]) * P["B0"]
+        Nc = (n // (P["ub1"] * P["s"])) * P["ub1"] * P["s"]
+        out["c"][:M, :Nc] = arr["c"][:M, :Nc] + arr["a"][:M, :K] @ arr["b"][:K, :Nc]
+    elif family == "jacobi":
+        N, t = P["N"], P["s"] * P["B"]
+        Pc = max(0, (N - 2) // t) * t
+        a = out["a"]
+        for step in range(P["T"]):
+            src, dst = (a[N:], a[:N]) if step % 2 == 0 else (a[:N], a[N:])
+            if Pc:
+                s = src[0:Pc] + src[1:Pc + 1] + src[2:Pc + 2]
+                dst[1:Pc + 1] = np.sign(s) * (np.abs(s) // 3)
+    return out
+
+
+@pytest.mark.parametrize("family", ["addition", "matvec", "matmul", "jacobi"])
+def test_random_wide_int_exact(cuda, family):
+    """ints whose results leave int32: the int64 kernels (never a wrapped
+    int32 result), exact against int64 arithmetic."""
+    from paper_1801_04348_b200 import last_run, marshal, programs, run_program
+
+    rng = np.random.default_rng(0x164 + 17 * sum(map(ord, family)) + 7919 * SEED)
+    kind = programs.original(family)
+    lim = {"addition": 2**40, "matvec": 2**24, "matmul": 2**24, "jacobi": 2**50}[family]
+    for _ in range(DRAWS):
+        P = _params(family, rng)
+        shapes = programs.array_shapes(kind, P)
+        arr = {k: rng.integers(-lim, lim, size=s, dtype=np.int64) for k, s in shapes.items()}
+        want = _restate_int(family, P, arr)
+        got = run_program(kind.text, P, {k: v.copy() for k, v in arr.items()})
+        srcs = {k: marshal.describe(k, v) for k, v in arr.items()}
+        wide = family == "jacobi" or marshal.int_bound(family, P, srcs) > marshal.I32_MAX
+        assert last_run().launch["dtype"] == ("i64" if wide else "i32"), (family, P)
+        for k in programs.FAMILIES[family].written:
+            assert np.array_equal(np.asarray(got[k]).reshape(-1), want[k].reshape(-1)), (family, P, k)
