@@ -31,7 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, binding, cases, marshal
-from .programs import FAMILIES, effective_params, identify
+from .programs import FAMILIES, c_div, effective_params, identify
 
 _INT32_MIN, _INT32_MAX = -(2**31), 2**31 - 1
 
@@ -595,13 +595,7 @@ def run_block(program, params, grid_values, context_values=None, arrays=None, tr
     return out
 
 
-def c_div(a: int, b: int) -> int:
-    """C99 truncating division (interp.py:43-46); the kernels use C '/'."""
-    q = abs(a) // abs(b)
-    return q if (a >= 0) == (b >= 0) else -q
-
-
-_c_div = c_div
+_c_div = c_div  # interp.py:43-46, defined once in programs.py
 
 
 def c_mod(a: int, b: int) -> int:

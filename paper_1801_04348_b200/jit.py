@@ -30,14 +30,15 @@ from . import _lib
 
 # ---------------------------------------------------------------- C exprs ----
 
+from .programs import c_div  # noqa: E402
+
 _TOK = re.compile(r"\s*(\d+|[A-Za-z_][A-Za-z_0-9]*|[-+*/%()])")
 
 
 def _c_div(a: int, b: int) -> int:
     if b == 0:
         raise ZeroDivisionError("division by zero in a binding (interp.py:43-46)")
-    q = abs(a) // abs(b)
-    return q if (a >= 0) == (b >= 0) else -q
+    return c_div(a, b)
 
 
 def ceval(text: str, env: dict) -> int:

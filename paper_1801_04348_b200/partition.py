@@ -35,9 +35,7 @@ ROW_FAMILIES = ("transpose", "matvec", "matmul", "addition")
 SHARDED_FAMILIES = ("reverse",) + ROW_FAMILIES  # run_rows
 
 
-def _c_div(a: int, b: int) -> int:
-    q = abs(a) // abs(b)
-    return q if (a >= 0) == (b >= 0) else -q
+from .programs import c_div as _c_div  # noqa: E402  (interp.py:43-46)
 
 
 def units(family: str, P: dict) -> tuple[int, int, int]:

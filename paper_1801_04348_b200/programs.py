@@ -60,10 +60,14 @@ def alpha(key: str) -> tuple[str, list[str]]:
     return " ".join(out), list(names)
 
 
-def _c_div(a: int, b: int) -> int:
-    """C99 truncating division (interp.py:43-46)."""
+def c_div(a: int, b: int) -> int:
+    """C99 truncating division (interp.py:43-46) -- the one definition the
+    package's host-side index arithmetic uses; the kernels use C '/'."""
     q = abs(a) // abs(b)
     return q if (a >= 0) == (b >= 0) else -q
+
+
+_c_div = c_div
 
 
 @dataclass(frozen=True)
