@@ -69,24 +69,6 @@ def _kind_of(value) -> str:
     return "list"
 
 
-def _list_dtype(data) -> str:
-    rows = data if data and isinstance(data[0], list) else [data]
-    for row in rows:
-        for v in row:
-            if isinstance(v, float):
-                return "f"
-    return "i"
-
-
-def _dtype_of(value) -> str:
-    k = _kind_of(value)
-    if k == "list":
-        return _list_dtype(value)
-    if k == "numpy":
-        return "f" if np.issubdtype(value.dtype, np.floating) else "i"
-    return "f" if value.dtype.is_floating_point else "i"
-
-
 def _numel(shape) -> int:
     n = 1
     for d in shape:
@@ -95,6 +77,9 @@ def _numel(shape) -> int:
 
 
 def _to_device_tensor(name, value, shape, np_dtype, device):
+    """int32 device copy of a caller's array for the emitted-leaf path
+    (jit.run_program_jit): IndexError when shorter than declared,
+    OverflowError outside int32 (the emitted leaves are C-int kernels)."""
     torch = _torch()
     k = _kind_of(value)
     want = _numel(shape)
@@ -132,19 +117,6 @@ def _to_device_tensor(name, value, shape, np_dtype, device):
         raise IndexError("array %s has %d elements; the program declares %s" % (name, flat.size, shape))
     host = torch.from_numpy(flat)
     return host.to(device, non_blocking=False), flat.size
-
-
-def _from_device(t, kind: str, shape, like):
-    if kind == "torch":
-        dev = like.device if like is not None else t.device
-        out = t.reshape(shape) if t.numel() == _numel(shape) else t
-        return out.to(dev)
-    host = t.cpu().numpy()
-    if host.size == _numel(shape):
-        host = host.reshape(shape)
-    if kind == "numpy":
-        return host.copy()
-    return host.tolist()
 
 
 def _shapes_py(fam, P):
