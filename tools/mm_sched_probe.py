@@ -1,7 +1,9 @@
 """Matmul schedules at n = 8192 and an 8-rank share: the order-preserving
 split (default) vs lockstep pieces (PK_MM_SCHED=pieces, PK_MM_PIECES=D,
 PK_MM_PGROUP=G); CUDA-event times and an exactness check (development probe;
-run under ncu --metrics dram__bytes_read.sum for the traffic)."""
+run under ncu --metrics dram__bytes_read.sum for the traffic).  The pieces
+schedule was measured slower and removed from the
+library; the environment variables are then ignored."""
 import os
 import sys
 
