@@ -757,9 +757,86 @@ def bench_kernels(peaks, mv, no_tune: bool = False, cpu: bool = True) -> dict:
                              "note": "float32 a, x, y; products split exactly and summed as a double-float pair"}
         del bufs, want
         torch.cuda.empty_cache()
+    out["matmul_n1024_table"] = bench_matmul_table(peaks, mv, threads if cpu else 0, no_tune)
     out["addition"] = bench_addition(peaks, mv, threads if cpu else 0)
     out["matmul_n2048"] = bench_matmul_n2048(peaks, mv, no_tune, threads if cpu else 0)
     return out
+
+
+# the paper's Table of matmul thread blocks (ub1, B0) x s
+PAPER_SHAPES = [(16, 4), (32, 4), (64, 4), (8, 8), (16, 8), (32, 8), (64, 8)]
+
+
+def bench_matmul_table(peaks, mv, threads: int, no_tune: bool = False) -> dict:
+    """BASELINE configs[0]: FP32 matmul n = 1024 with the case discussion
+    evaluated for the reference's default machine model (fermi.machine) at
+    the paper's Table shapes; each selected leaf runs on the B200 with the
+    program's own thread mapping (the generic kernel: a B0 x ub1 block per
+    B0 x ub1*s tile), beside the leaf the live machine tunes."""
+    import torch
+
+    from paper_1801_04348_b200 import _lib, binding, cases, programs
+
+    n = 1024
+    kind = programs.original("matmul")
+    g = torch.Generator(device="cuda").manual_seed(0x1801)
+    bufs = [torch.rand(n * n, device="cuda", generator=g) * 2 - 1 for _ in range(3)]
+    ptrs = [x.data_ptr() for x in bufs]
+    st = torch.cuda.current_stream()
+    peak = mv.props.get("sm_count", 148) * 256 * peaks["sm_max_mhz"] * 1e6 / 1e9
+    rows, worst = [], 0.0
+    for ub1, B0 in PAPER_SHAPES:
+        for s in (2, 4):
+            P = {"n": n, "B0": B0, "ub1": ub1, "s": s}
+            sel = cases.select(kind, P, "fermi")
+            L = binding.make_launch(kind, P, sel.applied, _lib.DTYPE_F32)
+            _lib.launch(L, ptrs, st.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(st)
+            for _ in range(5):
+                _lib.launch(L, ptrs, st.cuda_stream)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 5
+            bufs[2].zero_()
+            worst = max(worst, matmul_error(L, bufs, n, 0, n))
+            rows.append([ub1, B0, s, sel.index, list(sel.applied), round(2.0 * n ** 3 / (ms * 1e-3) / 1e9, 1)])
+    best = max(r[5] for r in rows)
+    # (B0, ub1, s) tuned inside the case the live machine selects (coverage-preserving candidates)
+    from paper_1801_04348_b200 import autotune
+
+    grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in ((64, 8, 8), (128, 8, 16), (64, 8, 16), (128, 8, 8))]
+    base = {"n": n, "B0": 64, "ub1": 8, "s": 8}
+    if no_tune:
+        P, trials = dict(base), []
+    else:
+        P, trials = autotune.autotune(kind, base, machine=mv, buffers=bufs, reps=5, grid=grid)
+    L = binding.make_launch(kind, P, cases.select(kind, P, mv).applied, _lib.DTYPE_F32)
+    _lib.launch(L, ptrs, st.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(10):
+        _lib.launch(L, ptrs, st.cuda_stream)
+    e1.record(st)
+    torch.cuda.synchronize()
+    tuned = 2.0 * n ** 3 / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e9
+    bufs[2].zero_()
+    worst = max(worst, matmul_error(L, bufs, n, 0, n))
+    del bufs
+    torch.cuda.empty_cache()
+    rec = {"value": round(tuned, 1), "unit": "GFLOP/s", "frac_of_fp32_peak": round(tuned / peak, 4),
+           "tuned_params": P, "paper_shapes": {"cols": ["ub1", "B0", "s", "fermi case", "applied", "GFLOP/s"],
+                                               "rows": rows, "best": best},
+           "parity": parity_text(worst, n),
+           "tuning_trials": len(trials),
+           "note": "every Table shape selects fermi case 1 (no strategies) at n = 1024, as the survey found; "
+                   "value = the leaf tuned inside the live B200's case; the Table shapes run the program's own "
+                   "thread mapping"}
+    if threads:
+        rec["cpu_baseline"] = cpu_matmul_rows(n, 0, n, threads)
+    return rec
 
 
 def bench_addition(peaks, mv, threads: int) -> dict:
