@@ -757,6 +757,8 @@ def bench_kernels(peaks, mv, no_tune: bool = False, cpu: bool = True) -> dict:
                              "note": "float32 a, x, y; products split exactly and summed as a double-float pair"}
         del bufs, want
         torch.cuda.empty_cache()
+        if cpu:
+            out["matvec_f32"]["cpu_baseline"] = cpu_matvec_f32(threads)
     out["matmul_n1024_table"] = bench_matmul_table(peaks, mv, threads if cpu else 0, no_tune)
     out["addition"] = bench_addition(peaks, mv, threads if cpu else 0)
     out["matmul_n2048"] = bench_matmul_n2048(peaks, mv, no_tune, threads if cpu else 0)
@@ -942,6 +944,25 @@ def parity_text(err: float, K: int) -> str:
     tol = max(1e-5 * K / 1024.0, 2.0 * K * 2.0**-24)
     return "%s: normalised error %.3g vs tolerance %.3g (1e-5*K/1024)" % ("within" if err <= tol else "MISMATCH",
                                                                          err, tol)
+
+
+def cpu_matvec_f32(threads: int) -> dict:
+    """float32 mat-vec by the oracle port (binary64 sums, all host threads) on
+    an N = 16384 sample of the N = 32768 workload, GB/s of a-traffic."""
+    import numpy as np
+
+    from oracle import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    N = 16384
+    rng = np.random.default_rng(0x1801)
+    arrays = {"a": rng.uniform(-1, 1, (N, N)).astype(np.float32), "x": rng.uniform(-1, 1, N).astype(np.float32)}
+    P = {"N": N, "s": 1, "B": 512}
+    oracle.run("matvec", P, arrays)
+    sec, runs = timed_cpu(lambda: oracle.run("matvec", P, arrays), budget_s=1.0)
+    return {"value": round((4 * N * N + 8 * N) / sec / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": "oracle/pk_oracle.c float32 mat-vec (binary64 sums) N=%d, %.3f s/run x %d" % (N, sec, runs)}
 
 
 def cpu_matmul_rows(n: int, r0: int, r1: int, threads: int) -> dict:
