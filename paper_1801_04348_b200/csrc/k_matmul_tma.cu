@@ -6,11 +6,18 @@
 // * a's rows of this launch are transposed once (k_transpose_rows, ~1 % of
 //   the multiply at n = 8192) so both operands are plain 2-D boxes: the
 //   a^T slab BK x BM and the b slab BK x BN of k-step kt are one TMA each.
-//   PK_MM_ROWA=1 instead loads a's rows as they lie (128-byte swizzled
-//   [BM][BK] box, 8 scalar shared loads per k step): no transpose launch and
-//   0.5 GB less DRAM traffic, but measured 12 % slower (19.3 vs 17.0 ms at
-//   n = 8192: the extra loads spill at the 128-register budget), so it is
-//   off by default.
+//   (Loading a's rows as they lie -- a 128-byte swizzled [BM][BK] box, 8
+//   scalar shared loads per k step -- saves the transpose launch and 0.5 GB
+//   of DRAM traffic but measured 12 % slower: 19.3 vs 17.0 ms at n = 8192,
+//   the extra loads spill at the 128-register budget.)
+// * Two tiles (template Tile), same thread mapping (8 x 8 outputs per
+//   thread) and numerics: 128 x 128 on 256 threads, 2 CTAs per SM, for the
+//   large matrices; 64 x 64 on 64 threads (16-deep slabs, up to 8 CTAs per
+//   SM), which the tuner picks for small ones (n = 1024: 64 tiles of 128 x 128
+//   leave most SMs idle; 34.7 against 31.9 TFLOP/s for the best other leaf).
+//   Measured and not used at n = 2048: 49.8 against 51.9 TFLOP/s -- the
+//   finer tiles would balance 1024 tiles over 148 SMs to 0.99, but the
+//   per-tile costs of a 2048-deep reduction on half-size slabs outweigh it.
 // * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage;
 //   thread 0 also issues the TMAs (a separate producer warp would push the
 //   block past the 2-blocks-per-SM register budget); the 8 compute warps
@@ -36,28 +43,28 @@
 namespace pk {
 namespace {
 
-constexpr int TY = 16, TX = 16;             // compute threads: 16 x 16, 8 x 8 outputs each
-constexpr int BM = 8 * TY, BN = 8 * TX;     // 128 x 128 block tile
-#ifndef PK_MM_BK
-#define PK_MM_BK 32
-#endif
-#ifndef PK_MM_STAGES
-#define PK_MM_STAGES 3
-#endif
 #ifndef PK_MM_AHEAD
 #define PK_MM_AHEAD 1
 #endif
-#ifndef PK_MM_ROWA
-#define PK_MM_ROWA 0
-#endif
-constexpr int BK = PK_MM_BK;                // k slab per stage
-constexpr int STAGES = PK_MM_STAGES;
-constexpr int AHEAD = PK_MM_AHEAD;          // slabs in flight ahead of the one computed on
-constexpr int NCOMP = TY * TX;              // 256 compute threads
-constexpr int NTHREADS = NCOMP;             // thread 0 also issues the TMAs
-constexpr int A_SLAB = BK * BM * 4, B_SLAB = BK * BN * 4;
-constexpr int STAGE_BYTES = A_SLAB + B_SLAB;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;
+constexpr int AHEAD = PK_MM_AHEAD;  // slabs in flight ahead of the one computed on
+
+template <int TY_, int TX_, int BK_, int STAGES_, int MINB_>
+struct Tile {
+    static constexpr int TY = TY_, TX = TX_;              // compute threads, 8 x 8 outputs each
+    static constexpr int BM = 8 * TY, BN = 8 * TX;        // block tile
+    static constexpr int BK = BK_;                        // k slab per stage
+    static constexpr int STAGES = STAGES_;
+    static constexpr int NCOMP = TY * TX;
+    static constexpr int NTHREADS = NCOMP;                // thread 0 also issues the TMAs
+    static constexpr int MINB = MINB_;                    // resident CTAs per SM
+    static constexpr int A_SLAB = BK * BM * 4, B_SLAB = BK * BN * 4;
+    static constexpr int STAGE_BYTES = A_SLAB + B_SLAB;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;  // ring + alignment + barriers
+};
+// BK = 32, 3 stages for the large tile (measured best, see above); the small
+// tile keeps 3 stages of 16-deep slabs (24 KB a CTA, 7 CTAs in 227 KB)
+using Big = Tile<16, 16, 32, 3, 2>;
+using Small = Tile<8, 8, 16, 3, 7>;
 
 // out[k][r] = a[r][k] for r < rows (row-major a with leading dimension lda)
 __global__ void __launch_bounds__(256) k_transpose_rows(const float *__restrict__ a, float *__restrict__ out,
@@ -104,24 +111,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // group wins: DRAM reads per launch 5.07 / 5.2 / 5.5 / 6.4 GB at GROUP 8 /
 // 12 / 16 / 20 with the split schedule, 3.50 / 3.43 / 3.48 / 3.82 GB without
 // it; the time is the same (FFMA-bound, 4 % of DRAM bandwidth).
+template <class C>
 __device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, int &m0, int &n0) {
     const int per_group = group * ntn;
     const int g = t / per_group, first = g * group;
     const int gsize = min(ntm - first, group);
     const int local = t - g * per_group;
-    m0 = (first + local % gsize) * BM;
+    m0 = (first + local % gsize) * C::BM;
     // odd groups walk the columns right to left (boustrophedon), so a window
     // straddling two groups shares the b panels at the turn
     const int col = local / gsize;
-    n0 = ((g & 1) ? ntn - 1 - col : col) * BN;
+    n0 = ((g & 1) ? ntn - 1 - col : col) * C::BN;
 }
 
 // Slabs [kb, ke) of tile (m0, n0): c rows -> packed accumulators, the ring,
 // accumulators -> c.  gs: this CTA's running slab count (the ring's stage and
 // barrier phase continue across work items).
+template <class T>
 __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtensorMap *map_b, float *__restrict__ C,
                                         int64_t ldc, int64_t rlo, int m0, int n0, int kb, int ke, int &gs,
                                         unsigned char *smem, uint64_t *full, uint64_t *empty) {
+    constexpr int TX = T::TX, BM = T::BM, BN = T::BN, BK = T::BK, STAGES = T::STAGES;
+    constexpr int STAGE_BYTES = T::STAGE_BYTES, A_SLAB = T::A_SLAB;
     const int tid = threadIdx.x;
     const int nk = ke - kb;
     // thread 0 doubles as the TMA producer: for slab j it refills the stage of
@@ -135,20 +146,13 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         fence_proxy_async();
         unsigned char *st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-#if PK_MM_ROWA
-        tma_load_2d(st, map_at, &full[s], (kb + j) * BK, m0);  // a rows as they lie: [BM rows][BK], 128B swizzle
-#else
         tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);
-#endif
         tma_load_2d(st + A_SLAB, map_b, &full[s], n0, (kb + j) * BK);
     };
     if (tid == 0)
         for (int j = 0; j < AHEAD && j < nk; j++) produce(j);
 
     const int tx = tid % TX, ty = tid / TX;
-#if PK_MM_ROWA
-    const int apar = (ty & 1) << 2, arow = ty * 4 * 128;
-#endif
     float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
     const int64_t chalf = (int64_t)(BM / 2) * ldc;
     // accumulators as packed column pairs: acc[i][jp] = {c[i][2jp], c[i][2jp+1]}
@@ -168,29 +172,11 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         mbar_wait(&full[s], (g / STAGES) & 1);
         const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
-#if PK_MM_ROWA
-        const unsigned char *Ab = smem + s * STAGE_BYTES;
-#endif
 #pragma unroll
         for (int kk = 0; kk < BK; kk++) {
-#if PK_MM_ROWA
-            // a slab [BM rows][32 k] with the 128-byte swizzle: element (r, k) at
-            // r*128 + ((k/4) ^ (r%8))*16 + (k%4)*4.  This thread's rows ty*4+i
-            // and BM/2+ty*4+i have r%8 = (i | 4*(ty&1)); the two rows a warp
-            // reads per load are 4 apart, so they land in different banks
-            const int c = kk >> 2;
-            float af[8];
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int chunk = (c ^ i ^ apar) << 4;
-                af[i] = *reinterpret_cast<const float *>(Ab + arow + i * 128 + chunk + (kk & 3) * 4);
-                af[4 + i] = *reinterpret_cast<const float *>(Ab + arow + (BM / 2 + i) * 128 + chunk + (kk & 3) * 4);
-            }
-#else
             const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
             const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
             const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#endif
             const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + tx * 4);
             const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + BN / 2 + tx * 4);
             const unsigned long long bp[4] = {b0.x, b0.y, b1.x, b1.y};
@@ -213,17 +199,19 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
     }
 }
 
+template <class T>
 __device__ __forceinline__ void mm_init(unsigned char *&smem, uint64_t *&full, uint64_t *&empty,
                                         unsigned char *smem_raw) {
+    constexpr int STAGES = T::STAGES;
     // align by offsetting the shared array itself (not via an integer cast), so
     // the compiler keeps the shared address space and emits LDS, not generic LD
     smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    full = reinterpret_cast<uint64_t *>(smem + STAGES * T::STAGE_BYTES);
     empty = full + STAGES;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCOMP / 32);
+            mbar_init(&empty[s], T::NCOMP / 32);
         }
         fence_mbar_init();
     }
@@ -231,17 +219,18 @@ __device__ __forceinline__ void mm_init(unsigned char *&smem, uint64_t *&full, u
 }
 
 // One 128 x 128 tile per CTA, the whole reduction.
-__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
+template <class T>
+__global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma(const __grid_constant__ CUtensorMap map_at,
                                                           const __grid_constant__ CUtensorMap map_b,
                                                           float *__restrict__ C, int64_t ldc, int64_t rlo,
                                                           int ntn, int ktiles, int group) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem;
     uint64_t *full, *empty;
-    mm_init(smem, full, empty, smem_raw);
+    mm_init<T>(smem, full, empty, smem_raw);
     int m0, n0, gs = 0;
-    tile_origin(blockIdx.x, (int)(gridDim.x / ntn), ntn, group, m0, n0);
-    mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
+    tile_origin<T>(blockIdx.x, (int)(gridDim.x / ntn), ntn, group, m0, n0);
+    mm_item<T>(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
 }
 
 // Persistent CTAs over an order-preserving split of the work (see
@@ -254,7 +243,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma(const __grid_constan
 // before it has stored c (the tile's progress word equals its first slab),
 // and every item publishes its last slab after storing.  c is the fp32
 // accumulator between the parts, so the bits equal one launch.
-__global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_constant__ CUtensorMap map_at,
+template <class T>
+__global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma_sched(const __grid_constant__ CUtensorMap map_at,
                                                                 const __grid_constant__ CUtensorMap map_b,
                                                                 float *__restrict__ C, int64_t ldc, int64_t rlo,
                                                                 int ntm, int ntn, int group, int base, int ktiles,
@@ -265,7 +255,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_c
     __shared__ int next;
     unsigned char *smem;
     uint64_t *full, *empty;
-    mm_init(smem, full, empty, smem_raw);
+    mm_init<T>(smem, full, empty, smem_raw);
     int gs = 0;
     for (;;) {
         if (threadIdx.x == 0) next = atomicAdd(ticket, 1);
@@ -274,13 +264,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_c
         __syncthreads();  // every thread has read next before thread 0 overwrites it
         if (t >= base) break;
         int m0, n0;
-        tile_origin(t, ntm, ntn, group, m0, n0);
-        mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
+        tile_origin<T>(t, ntm, ntn, group, m0, n0);
+        mm_item<T>(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
     }
     for (int it = off[blockIdx.x]; it < off[blockIdx.x + 1]; it++) {
         const int3 w = items[it];
         int m0, n0;
-        tile_origin(w.x, ntm, ntn, group, m0, n0);
+        tile_origin<T>(w.x, ntm, ntn, group, m0, n0);
         if (w.y > 0) {  // the tile's slabs before w.y are another CTA's: wait for their c
             if (threadIdx.x == 0) {
                 int v;
@@ -290,7 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) k_matmul_tma_sched(const __grid_c
             }
             __syncthreads();
         }
-        mm_item(&map_at, &map_b, C, ldc, rlo, m0, n0, w.y, w.z, gs, smem, full, empty);
+        mm_item<T>(&map_at, &map_b, C, ldc, rlo, m0, n0, w.y, w.z, gs, smem, full, empty);
         __syncthreads();  // every thread's c stores before the publication
         if (threadIdx.x == 0) {
             __threadfence();
@@ -334,10 +324,16 @@ int make_map(CUtensorMap *m, const float *base, int64_t rows, int64_t cols, int6
 
 }  // namespace
 
-// True when the TMA-fed kernel tiles this launch (128 x 128 block tile).
+// True when a TMA-fed kernel tiles this launch: the case's block tile is one
+// of the instantiated tiles (128 x 128 or 64 x 64) and divides the extents.
 bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n) {
-    return BM_case == BM && BN_case == BN && rows % BM == 0 && Nc % BN == 0 && K % BK == 0 && K > 0 &&
-           n % 4 == 0 && n <= ((int64_t)1 << 30);
+    auto fits = [&](int bm, int bn, int bk) {
+        // (K % 32: the a^T transpose works in 32 x 32 blocks)
+        return BM_case == bm && BN_case == bn && rows % bm == 0 && Nc % bn == 0 && K % bk == 0 && K % 32 == 0 &&
+               K > 0;
+    };
+    return (fits(Big::BM, Big::BN, Big::BK) || fits(Small::BM, Small::BN, Small::BK)) && n % 4 == 0 &&
+           n <= ((int64_t)1 << 30);
 }
 
 namespace {
@@ -413,27 +409,26 @@ int schedule_for(int dev, int64_t T, int64_t KS, int P, DevSched *out) {
 
 }  // namespace
 
-int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
-                      int64_t K, cudaStream_t st) {
+namespace {
+
+template <class C>
+int launch_tma_t(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc, int64_t K,
+                 cudaStream_t st) {
     const int64_t rows = rhi - rlo;
     float *at = nullptr;
     int rc = PK_OK;
     CUtensorMap mat, mb;
-#if PK_MM_ROWA
-    rc = make_map(&mat, a + rlo * n, rows, K, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
-#else
     cudaError_t e = scratch_alloc((void **)&at, (size_t)rows * K * sizeof(float), st);
     if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul a^T workspace: %s", cudaGetErrorString(e));
     k_transpose_rows<<<dim3((unsigned)(K / 32), (unsigned)(rows / 32)), 256, 0, st>>>(a + rlo * n, at, rows, K, n);
     rc = after_launch("matmul_transpose_a");
-    if (rc == PK_OK) rc = make_map(&mat, at, K, rows, rows, BM, BK);
-#endif
+    if (rc == PK_OK) rc = make_map(&mat, at, K, rows, rows, C::BM, C::BK);
     if (rc == PK_OK) {
-        if ((rc = make_map(&mb, b, K, Nc, n, BN, BK)) == PK_OK &&
-            (rc = allow_smem((const void *)k_matmul_tma, SMEM_BYTES)) == PK_OK &&
-            (rc = allow_smem((const void *)k_matmul_tma_sched, SMEM_BYTES)) == PK_OK) {
-            const int ntn = (int)(Nc / BN), ntm = (int)(rows / BM);
-            const int64_t T = (int64_t)ntm * ntn, KS = K / BK;
+        if ((rc = make_map(&mb, b, K, Nc, n, C::BN, C::BK)) == PK_OK &&
+            (rc = allow_smem((const void *)k_matmul_tma<C>, C::SMEM_BYTES)) == PK_OK &&
+            (rc = allow_smem((const void *)k_matmul_tma_sched<C>, C::SMEM_BYTES)) == PK_OK) {
+            const int ntn = (int)(Nc / C::BN), ntm = (int)(rows / C::BM);
+            const int64_t T = (int64_t)ntm * ntn, KS = K / C::BK;
             // rows of tiles per raster group (PK_MM_GROUP overrides: tuning aid)
             const char *genv = getenv("PK_MM_GROUP");
             const int group = genv && atoi(genv) > 0 ? atoi(genv) : PK_MM_GROUP;
@@ -441,7 +436,8 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
             int dev = 0, sms = 0, per_sm = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matmul_tma_sched, NTHREADS, SMEM_BYTES);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_matmul_tma_sched<C>, C::NTHREADS,
+                                                          C::SMEM_BYTES);
             const int64_t P = (int64_t)sms * per_sm;
             const bool split = getenv("PK_MM_NO_SPLIT") == nullptr && P > 0 && T > P && T % P != 0 && KS >= 8 &&
                                T * KS < ((int64_t)1 << 31);
@@ -449,25 +445,34 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
                 DevSched d;
                 int *progress = nullptr;  // T progress words, then the ticket counter
                 if ((rc = schedule_for(dev, T, KS, (int)P, &d)) == PK_OK) {
-                    cudaError_t e = scratch_alloc((void **)&progress, (size_t)(T + 1) * sizeof(int), st);
-                    if (e != cudaSuccess) rc = fail(PK_E_ALLOC, "matmul progress words: %s", cudaGetErrorString(e));
+                    cudaError_t e2 = scratch_alloc((void **)&progress, (size_t)(T + 1) * sizeof(int), st);
+                    if (e2 != cudaSuccess) rc = fail(PK_E_ALLOC, "matmul progress words: %s", cudaGetErrorString(e2));
                 }
                 if (rc == PK_OK) {
                     cudaMemsetAsync(progress, 0, (size_t)(T + 1) * sizeof(int), st);
-                    k_matmul_tma_sched<<<(unsigned)P, NTHREADS, SMEM_BYTES, st>>>(
+                    k_matmul_tma_sched<C><<<(unsigned)P, C::NTHREADS, C::SMEM_BYTES, st>>>(
                         mat, mb, c, n, rlo, ntm, ntn, group, (int)schedule_base(T, (int)P), (int)KS, d.items, d.off,
                         progress, progress + T);
                     rc = after_launch("matmul_tma_sched");
                     cudaFreeAsync(progress, st);
                 }
             } else {
-                k_matmul_tma<<<(unsigned)T, NTHREADS, SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn, (int)KS, group);
+                k_matmul_tma<C><<<(unsigned)T, C::NTHREADS, C::SMEM_BYTES, st>>>(mat, mb, c, n, rlo, ntn, (int)KS,
+                                                                                group);
                 rc = after_launch("matmul_tma");
             }
         }
     }
     if (at) cudaFreeAsync(at, st);
     return rc;
+}
+
+}  // namespace
+
+int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
+                      int64_t K, int tile, cudaStream_t st) {
+    if (tile == Small::BM) return launch_tma_t<Small>(a, b, c, n, rlo, rhi, Nc, K, st);
+    return launch_tma_t<Big>(a, b, c, n, rlo, rhi, Nc, K, st);
 }
 
 }  // namespace pk
