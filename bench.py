@@ -889,7 +889,7 @@ def bench_matmul_n2048(peaks, mv, no_tune: bool, threads: int) -> dict:
     base = {"n": n2, "B0": 128, "ub1": 8, "s": 16}
     g = torch.Generator(device="cuda").manual_seed(0x1801)
     bufs = [torch.rand(n2 * n2, device="cuda", generator=g) * 2 - 1 for _ in range(3)]
-    grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in ((128, 8, 16), (64, 8, 16), (64, 8, 8), (128, 8, 8))]
+    grid = [{"B0": B0, "ub1": ub1, "s": s} for B0, ub1, s in ((128, 8, 8), (128, 8, 16), (64, 8, 16), (64, 8, 8))]
     if no_tune:
         tuned, trials = dict(base), []
     else:

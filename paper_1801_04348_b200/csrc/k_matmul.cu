@@ -324,7 +324,7 @@ int launch_t(const pk_launch_t &L, void *const *p, cudaStream_t st, int64_t rlo,
         // 128 x 128 staged tile fed by TMA (same FFMA chain as the other kernels)
         if (L.variant == PK_VARIANT_STAGED && !generic && aligned16(a) && aligned16(b) && aligned16(c) &&
             matmul_tma_fits(L.B0, L.ub1 * elems(L), rhi - rlo, Nc, K, L.N) && rlo % 4 == 0)
-            return launch_matmul_tma(a, b, c, L.N, rlo, rhi, Nc, K, (int)L.B0, st);
+            return launch_matmul_tma(a, b, c, L.N, rlo, rhi, Nc, K, (int)L.B0, (int)(L.ub1 * elems(L)), st);
     }
     if constexpr (sizeof(T) == 4) {
         if (L.variant == PK_VARIANT_STAGED && !generic && L.N % 4 == 0 && K % 16 == 0 &&
@@ -412,7 +412,8 @@ int launch_matmul_kslice(const pk_launch_t &L, void *const *p, int64_t k0, int64
     const float *a = static_cast<const float *>(p[0]), *b = static_cast<const float *>(p[1]);
     float *c = static_cast<float *>(p[2]);
     if (!aligned16(a) || !aligned16(b) || !aligned16(c)) return fail(PK_E_UNSUPPORTED, "matmul: unaligned operands");
-    return launch_matmul_tma(a + k0, b + k0 * L.N, c, L.N, rlo, rhi, Nc, k1 - k0, (int)L.B0, st);
+    return launch_matmul_tma(a + k0, b + k0 * L.N, c, L.N, rlo, rhi, Nc, k1 - k0, (int)L.B0,
+                             (int)(L.ub1 * elems(L)), st);
 }
 
 }  // namespace pk

@@ -10,14 +10,28 @@
 //   scalar shared loads per k step -- saves the transpose launch and 0.5 GB
 //   of DRAM traffic but measured 12 % slower: 19.3 vs 17.0 ms at n = 8192,
 //   the extra loads spill at the 128-register budget.)
-// * Two tiles (template Tile), same thread mapping (8 x 8 outputs per
+// * Three tiles (template Tile), same thread mapping (8 x 8 outputs per
 //   thread) and numerics: 128 x 128 on 256 threads, 2 CTAs per SM, for the
-//   large matrices; 64 x 64 on 64 threads (16-deep slabs, up to 8 CTAs per
-//   SM), which the tuner picks for small ones (n = 1024: 64 tiles of 128 x 128
-//   leave most SMs idle; 34.7 against 31.9 TFLOP/s for the best other leaf).
-//   Measured and not used at n = 2048: 49.8 against 51.9 TFLOP/s -- the
-//   finer tiles would balance 1024 tiles over 148 SMs to 0.99, but the
-//   per-tile costs of a 2048-deep reduction on half-size slabs outweigh it.
+//   large matrices; 128 x 64 on 128 threads, 3 CTAs per SM, for n = 2048;
+//   64 x 64 on 64 threads (16-deep slabs, up to 8 CTAs per SM), which the
+//   tuner picks for small ones (n = 1024: 64 tiles of 128 x 128 leave most SMs
+//   idle; 34.7 against 31.9 TFLOP/s for the best other leaf).
+// * Why 128 x 64 at n = 2048.  The exact result forbids splitting a tile's
+//   reduction except in k order, so a tile's KS slabs run in sequence at one
+//   CTA's speed (1/c of an SM with c CTAs per SM); the order-preserving split
+//   below balances the SMs only when every run is at least one tile long, i.e.
+//   when there are at least 148 c tiles.  128 x 128 has 256 tiles for 296
+//   slots (0.865 balance at best); 128 x 64 has 512 for 444: split into equal
+//   runs of 1.15 tiles -> 57.2 against 51.8 TFLOP/s (tools/mm_kernel_probe.py).
+//   Measured and dropped: one CTA per SM with the whole register file
+//   (54.2 at n = 2048, 0.76 of peak at n = 8192: 8 warps do not cover the ring's
+//   waits); 256 x 128 on 512 threads (= Big at 2048, 0.860 at 8192); a's rows
+//   loaded as they lie through a 128-byte-swizzled box (no transpose launch) at
+//   255 / 170 registers: 10 % slower than the a^T slab at every size.
+// * The inner loop is at the FFMA2 ceiling of its instruction mix: the same
+//   loop with no barriers and no global traffic runs at 0.854 of peak with its
+//   operands from shared memory (0.985 from registers; 8 x 16 per thread
+//   0.874) -- tools/ffma2_probe.cu, profiles/r02_ffma2_ceiling.md.
 // * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage;
 //   thread 0 also issues the TMAs (a separate producer warp would push the
 //   block past the 2-blocks-per-SM register budget); the 8 compute warps
@@ -43,17 +57,13 @@
 namespace pk {
 namespace {
 
-#ifndef PK_MM_AHEAD
-#define PK_MM_AHEAD 1
-#endif
-constexpr int AHEAD = PK_MM_AHEAD;  // slabs in flight ahead of the one computed on
-
-template <int TY_, int TX_, int BK_, int STAGES_, int MINB_>
+template <int TY_, int TX_, int BK_, int STAGES_, int MINB_, int AHEAD_>
 struct Tile {
     static constexpr int TY = TY_, TX = TX_;              // compute threads, 8 x 8 outputs each
     static constexpr int BM = 8 * TY, BN = 8 * TX;        // block tile
     static constexpr int BK = BK_;                        // k slab per stage
     static constexpr int STAGES = STAGES_;
+    static constexpr int AHEAD = AHEAD_;                  // slabs in flight ahead of the one computed on
     static constexpr int NCOMP = TY * TX;
     static constexpr int NTHREADS = NCOMP;                // thread 0 also issues the TMAs
     static constexpr int MINB = MINB_;                    // resident CTAs per SM
@@ -61,10 +71,12 @@ struct Tile {
     static constexpr int STAGE_BYTES = A_SLAB + B_SLAB;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;  // ring + alignment + barriers
 };
-// BK = 32, 3 stages for the large tile (measured best, see above); the small
-// tile keeps 3 stages of 16-deep slabs (24 KB a CTA, 7 CTAs in 227 KB)
-using Big = Tile<16, 16, 32, 3, 2>;
-using Small = Tile<8, 8, 16, 3, 7>;
+// BK = 32, 3 stages, 1 slab ahead for the two-per-SM tile (measured best, see
+// above); the small tile keeps 3 stages of 16-deep slabs (24 KB a CTA, 7 CTAs
+// in 227 KB); Mid: 128 x 64 on 128 threads, 3 CTAs per SM (72 KB rings).
+using Big = Tile<16, 16, 32, 3, 2, 1>;
+using Small = Tile<8, 8, 16, 3, 7, 1>;
+using Mid = Tile<16, 8, 32, 3, 3, 1>;
 
 // out[k][r] = a[r][k] for r < rows (row-major a with leading dimension lda)
 __global__ void __launch_bounds__(256) k_transpose_rows(const float *__restrict__ a, float *__restrict__ out,
@@ -131,7 +143,7 @@ template <class T>
 __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtensorMap *map_b, float *__restrict__ C,
                                         int64_t ldc, int64_t rlo, int m0, int n0, int kb, int ke, int &gs,
                                         unsigned char *smem, uint64_t *full, uint64_t *empty) {
-    constexpr int TX = T::TX, BM = T::BM, BN = T::BN, BK = T::BK, STAGES = T::STAGES;
+    constexpr int TX = T::TX, BM = T::BM, BN = T::BN, BK = T::BK, STAGES = T::STAGES, AHEAD = T::AHEAD;
     constexpr int STAGE_BYTES = T::STAGE_BYTES, A_SLAB = T::A_SLAB;
     const int tid = threadIdx.x;
     const int nk = ke - kb;
@@ -332,7 +344,8 @@ bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc,
         return BM_case == bm && BN_case == bn && rows % bm == 0 && Nc % bn == 0 && K % bk == 0 && K % 32 == 0 &&
                K > 0;
     };
-    return (fits(Big::BM, Big::BN, Big::BK) || fits(Small::BM, Small::BN, Small::BK)) && n % 4 == 0 &&
+    return (fits(Big::BM, Big::BN, Big::BK) || fits(Small::BM, Small::BN, Small::BK) ||
+            fits(Mid::BM, Mid::BN, Mid::BK)) && n % 4 == 0 &&
            n <= ((int64_t)1 << 30);
 }
 
@@ -470,8 +483,9 @@ int launch_tma_t(const float *a, const float *b, float *c, int64_t n, int64_t rl
 }  // namespace
 
 int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
-                      int64_t K, int tile, cudaStream_t st) {
-    if (tile == Small::BM) return launch_tma_t<Small>(a, b, c, n, rlo, rhi, Nc, K, st);
+                      int64_t K, int bm, int bn, cudaStream_t st) {
+    if (bm == Small::BM && bn == Small::BN) return launch_tma_t<Small>(a, b, c, n, rlo, rhi, Nc, K, st);
+    if (bm == Mid::BM && bn == Mid::BN) return launch_tma_t<Mid>(a, b, c, n, rlo, rhi, Nc, K, st);
     return launch_tma_t<Big>(a, b, c, n, rlo, rhi, Nc, K, st);
 }
 

@@ -174,7 +174,7 @@ int launch_matvec(const pk_launch_t &L, void *const *p, cudaStream_t st);
 int launch_matmul(const pk_launch_t &L, void *const *p, cudaStream_t st);
 bool matmul_tma_fits(int64_t BM_case, int64_t BN_case, int64_t rows, int64_t Nc, int64_t K, int64_t n);
 int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
-                      int64_t K, int tile, cudaStream_t st);
+                      int64_t K, int bm, int bn, cudaStream_t st);
 bool matmul_kslice_ok(const pk_launch_t &L, int64_t slice);
 int launch_matmul_kslice(const pk_launch_t &L, void *const *p, int64_t k0, int64_t k1, cudaStream_t st);
 int launch_matmul_tf32x3(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi,

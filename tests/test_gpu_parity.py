@@ -216,8 +216,9 @@ def test_tuned_and_generic_matmul_bit_identical(cuda):
     n = 256
     rng = np.random.default_rng(5)
     arrays = {k: rng.standard_normal((n, n)).astype(np.float32) for k in "abc"}
-    # 64 x 64 register-blocked tile; 128 x 128 TMA-fed tile (packed f32x2 FMAs)
-    for params in ({"n": n, "B0": 64, "ub1": 8, "s": 8}, {"n": n, "B0": 128, "ub1": 8, "s": 16}):
+    # 64 x 64 register-blocked tile; 128 x 128 and 128 x 64 TMA-fed tiles (packed f32x2 FMAs)
+    for params in ({"n": n, "B0": 64, "ub1": 8, "s": 8}, {"n": n, "B0": 128, "ub1": 8, "s": 16},
+                   {"n": n, "B0": 128, "ub1": 8, "s": 8}):
         t = _run(programs.source("matmul"), params, arrays)["c"]
         g = _run(programs.source("matmul"), params, arrays, generic=True)["c"]
         assert np.array_equal(t.view(np.uint32), g.view(np.uint32)), params
@@ -384,6 +385,41 @@ def test_matmul_split_schedule_exact_on_row_shares(cuda, rows):
     torch.cuda.synchronize()
     assert torch.equal(got[lo:hi].double(), want)
     assert torch.equal(got[:lo], c[:lo]) and torch.equal(got[hi:], c[hi:])
+
+
+@pytest.mark.parametrize("rows", [(0, 2048), (0, 1024), (512, 1920)])
+def test_matmul_mid_tile_split_bit_identical(cuda, rows):
+    """n = 2048 on the 128 x 64 TMA tile (3 CTAs per SM): 512 tiles for 444
+    slots take the order-preserving split with every tile cut; random fp32 in
+    [-1, 1): the bits must equal the 128 x 128 tile's and the generic kernel's
+    (one ascending-k fma chain per output), rows outside the share untouched."""
+    torch = cuda
+    from paper_1801_04348_b200 import _lib, binding, programs
+
+    n = 2048
+    lo, hi = rows
+    g = torch.Generator(device="cuda").manual_seed(hi)
+    a, b, c = (torch.rand(n * n, device="cuda", generator=g) * 2 - 1 for _ in range(3))
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for params, generic in (({"n": n, "B0": 128, "ub1": 8, "s": 8}, False),
+                            ({"n": n, "B0": 128, "ub1": 8, "s": 16}, False),
+                            ({"n": n, "B0": 128, "ub1": 8, "s": 16}, True)):
+        L = binding.make_launch(programs.original("matmul"), params, (), _lib.DTYPE_F32, lo=lo, hi=hi,
+                                generic=generic)
+        for rep in range(3):  # repeated launches: the split's waits and refills race for real
+            got = c.clone()
+            _lib.launch(L, [a.data_ptr(), b.data_ptr(), got.data_ptr()], st)
+            torch.cuda.synchronize()
+            if outs:
+                assert torch.equal(got.view(torch.int32), outs[0].view(torch.int32)), (params, generic, rep)
+            else:
+                outs.append(got)
+    got = outs[0].view(n, n)
+    want = c.view(n, n)[lo:hi].double() + a.view(n, n)[lo:hi].double() @ b.view(n, n).double()
+    scale = (a.view(n, n)[lo:hi].double().abs() @ b.view(n, n).double().abs()).max()
+    assert ((got[lo:hi].double() - want).abs().max() / scale).item() <= _matmul_tol(n)
+    assert torch.equal(got[:lo], c.view(n, n)[:lo]) and torch.equal(got[hi:], c.view(n, n)[hi:])
 
 
 @pytest.mark.parametrize("N,scale", [(32768, 1.0), (4099, 1e30), (777, 1e-30)])
