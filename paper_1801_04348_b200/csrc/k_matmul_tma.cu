@@ -27,7 +27,9 @@
 //   (54.2 at n = 2048, 0.76 of peak at n = 8192: 8 warps do not cover the ring's
 //   waits); 256 x 128 on 512 threads (= Big at 2048, 0.860 at 8192); a's rows
 //   loaded as they lie through a 128-byte-swizzled box (no transpose launch) at
-//   255 / 170 registers: 10 % slower than the a^T slab at every size.
+//   255 / 170 registers: 10 % slower than the a^T slab at every size; 8 x 16
+//   outputs per thread (128 threads, 200 registers, 2 CTAs per SM): 0.830 of
+//   peak at n = 8192 against 0.876, although its bare loop is 2 % faster.
 // * The inner loop is at the FFMA2 ceiling of its instruction mix: the same
 //   loop with no barriers and no global traffic runs at 0.854 of peak with its
 //   operands from shared memory (0.985 from registers; 8 x 16 per thread
