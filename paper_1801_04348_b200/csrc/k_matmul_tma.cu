@@ -29,7 +29,11 @@
 //   loaded as they lie through a 128-byte-swizzled box (no transpose launch) at
 //   255 / 170 registers: 10 % slower than the a^T slab at every size; 8 x 16
 //   outputs per thread (128 threads, 200 registers, 2 CTAs per SM): 0.830 of
-//   peak at n = 8192 against 0.876, although its bare loop is 2 % faster.
+//   peak at n = 8192 against 0.876, although its bare loop is 2 % faster;
+//   8 x 4 per thread (more warps for small n: 128 x 64 on 256 threads, 64 x 64
+//   on 128) 38.6 / 36.0 TFLOP/s at n = 1024 against 38.4 for the 128 x 64 tile
+//   -- n = 1024 has 2^20 outputs, 4 warps of 8 x 8 per SM: the few warps, not
+//   the blocking, set its rate.
 // * The inner loop is at the FFMA2 ceiling of its instruction mix: the same
 //   loop with no barriers and no global traffic runs at 0.854 of peak with its
 //   operands from shared memory (0.985 from registers; 8 x 16 per thread

@@ -14,13 +14,14 @@ __device__ __forceinline__ void fma2p(unsigned long long &c, unsigned long long 
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
 }
 
-template <bool SMEM, int MINB, int RM, int RN>
-__global__ void __launch_bounds__(256, MINB) k(float *out, int iters) {
-    constexpr int BM = 16 * RM, BN = 16 * RN;
+template <bool SMEM, int MINB, int RM, int RN, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k(float *out, int iters) {
+    constexpr int TX = 16, TY = NT / 16;
+    constexpr int BM = TY * RM, BN = TX * RN;
     extern __shared__ __align__(16) float sm[];
     float *As = sm, *Bs = sm + 32 * BM;
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    for (int i = tid; i < 32 * (BM + BN); i += 256) sm[i] = 1e-3f * (i % 7);
+    for (int i = tid; i < 32 * (BM + BN); i += NT) sm[i] = 1e-3f * (i % 7);
     __syncthreads();
     unsigned long long acc[RM][RN / 2];
 #pragma unroll
@@ -60,39 +61,39 @@ __global__ void __launch_bounds__(256, MINB) k(float *out, int iters) {
     for (int i = 0; i < RM; i++)
 #pragma unroll
         for (int j = 0; j < RN / 2; j++) s += __uint_as_float((unsigned)acc[i][j]);
-    out[blockIdx.x * 256 + tid] = s;
+    out[blockIdx.x * NT + tid] = s;
 }
 
-template <bool SMEM, int MINB, int RM, int RN>
-void run(const char *name, int per_sm, int sms, float *out) {
-    const int iters = 1000, blocks = sms * per_sm;
-    const int smem = 32 * 16 * (RM + RN) * 4;
-    cudaFuncSetAttribute(k<SMEM, MINB, RM, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<SMEM, MINB, RM, RN><<<blocks, 256, smem>>>(out, 10);
+template <bool SMEM, int MINB, int RM, int RN, int NT = 256>
+void run(const char *name, int per_sm, int sms, float *out, int blocks_override = 0) {
+    const int iters = 1000, blocks = blocks_override ? blocks_override : sms * per_sm;
+    const int smem = 32 * ((NT / 16) * RM + 16 * RN) * 4;
+    cudaFuncSetAttribute(k<SMEM, MINB, RM, RN, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<SMEM, MINB, RM, RN, NT><<<blocks, 256, smem>>>(out, 10);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k<SMEM, MINB, RM, RN><<<blocks, 256, smem>>>(out, iters);
+    k<SMEM, MINB, RM, RN, NT><<<blocks, 256, smem>>>(out, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double flop = 2.0 * blocks * 256.0 * iters * 32 * RM * RN;
+    const double flop = 2.0 * blocks * (double)NT * iters * 32 * RM * RN;
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const double peak = sms * 256.0 * clk * 1e3;
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k<SMEM, MINB, RM, RN>);
-    printf("%-10s %2dx%-2d %d CTA/SM (%3d regs): %.2f TFLOP/s = %.3f of %.2f (max clock)\n", name, RM, RN, per_sm,
-           fa.numRegs, flop / ms / 1e9, flop / ms * 1e3 / peak, peak / 1e12);
+    cudaFuncGetAttributes(&fa, k<SMEM, MINB, RM, RN, NT>);
+    printf("%-10s %2dx%-2d %3d thr %4d CTAs (%3d regs): %.2f TFLOP/s = %.3f of %.2f (max clock)\n", name, RM, RN, NT,
+           blocks, fa.numRegs, flop / ms / 1e9, flop / ms * 1e3 / peak, peak / 1e12);
 }
 
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float *out;
-    cudaMalloc(&out, sms * 4 * 256 * 4);
+    cudaMalloc(&out, (1 << 20) * 4);
     run<false, 2, 8, 8>("registers", 2, sms, out);
     run<true, 2, 8, 8>("smem", 2, sms, out);
     run<true, 1, 8, 8>("smem", 1, sms, out);
@@ -100,6 +101,15 @@ int main() {
     run<true, 1, 16, 8>("smem", 1, sms, out);
     run<true, 1, 12, 8>("smem", 1, sms, out);
     run<true, 1, 8, 12>("smem", 1, sms, out);
+    // n = 1024: 2^20 outputs in all; threads = 2^20 / (RM * RN)
+    printf("n = 1024 (2^20 outputs):\n");
+    run<true, 1, 8, 8, 64>("smem", 0, sms, out, (1 << 20) / 64 / 64);
+    run<true, 1, 8, 8, 128>("smem", 0, sms, out, (1 << 20) / 64 / 128);
+    run<true, 1, 4, 8, 128>("smem", 0, sms, out, (1 << 20) / 32 / 128);
+    run<true, 1, 4, 8, 256>("smem", 0, sms, out, (1 << 20) / 32 / 256);
+    run<true, 1, 4, 4, 128>("smem", 0, sms, out, (1 << 20) / 16 / 128);
+    run<true, 1, 4, 4, 256>("smem", 0, sms, out, (1 << 20) / 16 / 256);
+    run<true, 1, 8, 4, 256>("smem", 0, sms, out, (1 << 20) / 32 / 256);
     printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
 }
