@@ -103,11 +103,7 @@ int main() {
     run<true, 1, 8, 12>("smem", 1, sms, out);
     // n = 1024: 2^20 outputs in all; threads = 2^20 / (RM * RN)
     printf("n = 1024 (2^20 outputs):\n");
-    run<true, 1, 8, 8, 64>("smem", 0, sms, out, (1 << 20) / 64 / 64);
-    run<true, 1, 8, 8, 128>("smem", 0, sms, out, (1 << 20) / 64 / 128);
-    run<true, 1, 4, 8, 128>("smem", 0, sms, out, (1 << 20) / 32 / 128);
     run<true, 1, 4, 8, 256>("smem", 0, sms, out, (1 << 20) / 32 / 256);
-    run<true, 1, 4, 4, 128>("smem", 0, sms, out, (1 << 20) / 16 / 128);
     run<true, 1, 4, 4, 256>("smem", 0, sms, out, (1 << 20) / 16 / 256);
     run<true, 1, 8, 4, 256>("smem", 0, sms, out, (1 << 20) / 32 / 256);
     printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
