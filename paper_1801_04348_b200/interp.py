@@ -173,6 +173,7 @@ def run_program(
     temporal: int = 0,
     devices=None,
     halo: int = 0,
+    via_generic: bool = False,
 ) -> dict:
     """Execute the whole program on the GPU; returns the final array contents.
 
@@ -196,6 +197,9 @@ def run_program(
     ``devices=[d0, d1, ...]``: run on several GPUs of this process
     (pk_launch_multi: unit shares, ghost-zone exchange of width ``halo``
     by peer copies for the stencils); the result is gathered on ``d0``.
+    ``via_generic``: run the program through the generic path (generic.py:
+    any program, our emitted kernel) even when it is one of the families --
+    the path programs outside the families take.
     """
     global _last
     if tracer is not None:
@@ -203,20 +207,27 @@ def run_program(
             "tracer is CPU-only instrumentation of the reference interpreter; "
             "the GPU executor cannot report per-access events"
         )
-    try:
-        kind = identify(program)
-    except NotImplementedError:
-        # outside the seven families: compile the reference's own emitted leaf
-        # for sm_100a (NVRTC) when parakern is here to emit it (jit.py)
-        if not (hasattr(program, "decls") and hasattr(program, "top")):
-            raise
-        from . import jit
+    if via_generic:
+        kind = None
+    else:
+        try:
+            kind = identify(program)
+        except NotImplementedError:
+            kind = None
+    if kind is None:
+        # outside the seven families (or asked for): the generic path -- our
+        # parser and CUDA emitter, NVRTC for sm_100a, the interpreter's value
+        # semantics (generic.py); no parakern needed
+        from . import generic
+        from .programs import program_text
 
-        warnings.warn("program matches none of the seven kernel families: running the reference emitter's "
-                      "leaf compiled with NVRTC (no hand-written kernel)", RuntimeWarning, stacklevel=2)
-        leaf = jit.emit_leaf(program, params)
-        _last = RunInfo("emitted", None, tuple(leaf.applied), False, {"kernel": leaf.kernel_name}, 0)
-        return jit.run_program_jit(leaf, params, arrays)
+        if not via_generic:
+            warnings.warn("program matches none of the seven kernel families: running it through the generic "
+                          "emitted kernel (no hand-written kernel)", RuntimeWarning, stacklevel=2)
+        out = generic.run_program(program_text(program), params, arrays, device=device)
+        g = generic.last
+        _last = RunInfo("generic", None, (), False, {"mode": g.mode, "flat": g.flat, "launches": g.launches}, 0)
+        return out
     rename = dict(kind.rename)
     if rename:  # an alpha-renamed copy of a known program: speak the family's names inside
         params = {rename.get(k, k): v for k, v in params.items()}

@@ -14,7 +14,7 @@ cap() {  # name regex skip args...
   echo "$name rc=$?"
 }
 cap matmul k_matmul_tma_sched 1 matmul '{"n": 8192, "B0": 128, "ub1": 8, "s": 16}' 3
-cap matmul_n2048 'k_matmul_tma$' 1 matmul '{"n": 2048, "B0": 128, "ub1": 8, "s": 16}' 3
+cap matmul_n2048 k_matmul_tma_sched 1 matmul '{"n": 2048, "B0": 128, "ub1": 8, "s": 8}' 3
 cap tf32x3 k_tf32x3 1 matmul '{"n": 8192, "B0": 128, "ub1": 8, "s": 16}' 3 --tf32x3
 cap jacobi1d k_jacobi1d_reg 3 jacobi '{"T": 4, "N": 268435458, "s": 16, "B": 256}' 1
 cap jacobi2d k_jacobi2d_reg 3 jacobi2d '{"T": 4, "N": 16386, "s": 32, "B0": 64, "B1": 4}' 1
@@ -27,7 +27,7 @@ cap matvec k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 512}' 3
 cap matvec_f32 k_matvec 1 matvec '{"N": 32768, "s": 1, "B": 512}' 3 --f32
 cap addition k_addition_vec 1 addition '{"N": 16384, "B0": 8, "B1": 128}' 3
 cap temporal k_jacobi1d_rtemporal 0 jacobi '{"T": 16, "N": 268435458, "s": 16, "B": 256}' 1 --temporal=15
-cap matmul_f64 k_matmul_generic 1 matmul '{"n": 2048, "B0": 32, "ub1": 8, "s": 4}' 3 --f64
+cap matmul_f64 k_matmul_exact_tiled 1 matmul '{"n": 2048, "B0": 32, "ub1": 8, "s": 4}' 3 --f64
 cap matvec_f64 k_matvec_exact 1 matvec '{"N": 32768, "s": 1, "B": 512}' 3 --f64
 cap reverse_f64 k_reverse 1 reverse '{"N": 536870912, "s": 16, "B": 256}' 3 --f64
 ls -la $D
