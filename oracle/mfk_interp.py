@@ -184,3 +184,13 @@ def run_program(prog, params, arrays=None, stats=None, all_iterations=False):
         if stats is not None:
             stats["wide"] = m.wide
     return m.arrays
+
+
+def run_block(prog, params, grid_values, context_values=None, arrays=None):
+    """interp.run_block (interp.py:228-249): declarations, then the context and
+    grid values set, then the thread loops swept over the body."""
+    m = _Machine(prog, params, arrays)
+    m.env.update(context_values or {})
+    m.env.update(grid_values)
+    m.nest(list(prog.thread), prog.body)
+    return m.arrays

@@ -556,10 +556,32 @@ def _pinned_buffer(nbytes: int):
 
 def run_program(program_text: str, params: dict, arrays: dict | None = None, *, device=None) -> dict:
     """interp.run_program for any parsed program, on the GPU (see the module doc)."""
+    return _run(mfk.parse(program_text), params, arrays, device, None)
+
+
+def run_block(program_text: str, params: dict, grid_values: dict, context_values: dict | None = None,
+              arrays: dict | None = None, *, device=None) -> dict:
+    """interp.run_block (interp.py:228-249) for any parsed program: the
+    declarations with ``params``, then the context and grid values set, then
+    the thread loops swept (the grid loops are not run); an access outside an
+    array raises IndexError, a name without a value KeyError."""
+    import copy
+
+    prog = mfk.parse(program_text)
+    if len(prog.grid) > 2 or len(prog.thread) > 2:  # dsl.split_roles (dsl.py:651-656)
+        raise mfk.MfkError("at most two grid and two thread dimensions are supported (got %d grid, %d thread)"
+                           % (len(prog.grid), len(prog.thread)))
+    block = copy.copy(prog)
+    block.meta, block.grid, block.thread, block.context = list(prog.thread), [], list(prog.thread), []
+    extra = dict(context_values or {})
+    extra.update(grid_values)
+    return _run(block, params, arrays, device, extra)
+
+
+def _run(prog: mfk.Program, params: dict, arrays, device, extra) -> dict:
     global last
     import torch
 
-    prog = mfk.parse(program_text)
     if not torch.cuda.is_available():
         raise RuntimeError("run_program needs a CUDA device (sm_100a); there is no CPU fallback")
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
@@ -574,6 +596,8 @@ def run_program(program_text: str, params: dict, arrays: dict | None = None, *, 
             dims[name] = tuple(host_eval(d, env) for d in prog.arrays[name])
         elif name not in env:
             raise KeyError("no value supplied for parameter %r" % name)
+    if extra:  # run_block: context and grid values after the declarations (interp.py:244-245)
+        env.update(extra)
     used = set(prog.scalars) | {b for b, _ in prog.bindings}
     for e in mfk.walk_exprs((prog.body, tuple(b for _, b, _ in prog.meta), tuple(b for _, b in prog.context))):
         if e[0] == "name":

@@ -510,7 +510,17 @@ def run_block(program, params, grid_values, context_values=None, arrays=None, tr
             "tracer is CPU-only instrumentation of the reference interpreter; "
             "the GPU executor cannot report per-access events"
         )
-    kind = identify(program)
+    try:
+        kind = identify(program)
+    except NotImplementedError:
+        # outside the seven families: one block of the generic path's kernel
+        from . import generic
+        from .programs import program_text
+
+        out = generic.run_block(program_text(program), params, grid_values, context_values, arrays)
+        g = generic.last
+        _last = RunInfo("generic", None, (), False, {"mode": g.mode, "block": True, "launches": g.launches}, 0)
+        return out
     rename = dict(kind.rename)
     grid_values = {rename.get(k, k): v for k, v in dict(grid_values).items()}
     context_values = {rename.get(k, k): v for k, v in dict(context_values or {}).items()}

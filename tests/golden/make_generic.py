@@ -265,6 +265,29 @@ def main() -> int:
                 entry["missing_param"] = None
             except KeyError:
                 entry["missing_param"] = {"drop": drop, "error": "KeyError"}
+        # run_block (interp.py:228-249): grid values fixed, thread loops swept
+        try:
+            grid, _ = dsl.split_roles(prog)
+        except dsl.DslError:
+            grid = None
+        if grid is not None and len(vectors) < 40:
+            from parakern import interp
+
+            entry["blocks"] = []
+            arrays = value_inputs(rng, prog, params, "int")
+            for pick in ("zero", "inside", "past"):
+                gv = {}
+                for m in grid:
+                    bound = interp.Machine(prog, dict(params)).eval(m.bound) if not any(
+                        x.var in dsl._names_in(m.bound) for x in prog.meta_loops()) else 1
+                    gv[m.var] = {"zero": 0, "inside": rng.randrange(max(bound, 1)), "past": max(bound, 0) + 1}[pick]
+                cv = {c.var: rng.randrange(2) for c in prog.context_loops}
+                try:
+                    out = interp.run_block(prog, dict(params), gv, cv, arrays=json.loads(json.dumps(arrays)))
+                    res = {"outputs": out}
+                except (IndexError, ZeroDivisionError, KeyError, TypeError) as exc:
+                    res = {"error": type(exc).__name__}
+                entry["blocks"].append(dict(res, grid_values=gv, context_values=cv, inputs=arrays))
         vectors.append(entry)
     for text in BAD:
         try:

@@ -134,3 +134,21 @@ def test_host_eval_is_c_division():
         generic.host_eval(("bin", "/", ("num", 1), ("num", 0)), {})
     with pytest.raises(KeyError):
         generic.host_eval(("name", "missing"), {})
+
+
+def test_oracle_run_block_equals_the_reference(golden):
+    n = 0
+    for entry in golden["programs"]:
+        prog = mfk.parse(entry["text"])
+        for b in entry.get("blocks", ()):
+            args = (prog, dict(entry["params"]), b["grid_values"], b["context_values"],
+                    json.loads(json.dumps(b["inputs"])))
+            if "error" in b:
+                with pytest.raises(eval(b["error"])):
+                    mfk_interp.run_block(*args)
+            else:
+                got = mfk_interp.run_block(*args)
+                for k in b["outputs"]:
+                    assert same(got[k], b["outputs"][k]), (entry["name"], k)
+            n += 1
+    assert n >= 100

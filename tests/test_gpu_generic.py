@@ -197,3 +197,29 @@ def test_random_programs_against_the_restated_interpreter(cuda, seed):
         except (IndexError, ZeroDivisionError, KeyError, TypeError) as exc:
             want, err = None, type(exc).__name__
         _check(text, params, arrays, want, err)
+
+
+def test_run_block_matches_the_reference(cuda, golden):
+    """run_block of programs outside the families (generic.run_block): the
+    reference's arrays, or its IndexError past the grid."""
+    import warnings
+
+    from paper_1801_04348_b200 import last_run, run_block
+
+    n = 0
+    for entry in golden["programs"]:
+        for b in entry.get("blocks", ()):
+            args = (entry["text"], dict(entry["params"]), b["grid_values"], b["context_values"],
+                    json.loads(json.dumps(b["inputs"])))
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                if "error" in b:
+                    with pytest.raises(ERRORS[b["error"]]):
+                        run_block(*args)
+                else:
+                    got = run_block(*args)
+                    assert last_run().family == "generic"
+                    for k in b["outputs"]:
+                        assert same(got[k], b["outputs"][k]), (entry["name"], k)
+            n += 1
+    assert n >= 100
