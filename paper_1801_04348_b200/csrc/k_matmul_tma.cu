@@ -34,10 +34,26 @@
 //   on 128) 38.6 / 36.0 TFLOP/s at n = 1024 against 38.4 for the 128 x 64 tile
 //   -- n = 1024 has 2^20 outputs, 4 warps of 8 x 8 per SM: the few warps, not
 //   the blocking, set its rate.
-// * The inner loop is at the FFMA2 ceiling of its instruction mix: the same
-//   loop with no barriers and no global traffic runs at 0.854 of peak with its
-//   operands from shared memory (0.985 from registers; 8 x 16 per thread
-//   0.874) -- tools/ffma2_probe.cu, profiles/r02_ffma2_ceiling.md.
+// * Issue order of the FFMA2s.  An FFMA2 with a scalar a, a b pair and a c pair
+//   reads up to 5 registers; when neither the a nor the b operand carries over
+//   from the previous instruction (operand reuse cache) one register bank is
+//   read three times and the instruction takes an extra cycle.  Writing the
+//   k step b-pair-major (each b pair meets the 8 a values in a row) lets ptxas
+//   keep the pair in the reuse cache: the bare loop (no barriers, no global
+//   traffic, operands from shared memory) runs at 0.923 of the FFMA peak
+//   against 0.858 a-major (0.985 with operands in registers) --
+//   tools/ffma2_order_probe.cu, tools/ffma2_probe.cu,
+//   profiles/r02_ffma2_ceiling.md.  In the kernels: Mid 0.843 -> 0.873-0.886
+//   at n = 8192, 0.769 -> 0.79-0.80 at n = 2048; Big unchanged (0.86-0.87,
+//   124 of its 128 registers).
+// * ROWA tiles (PK_MM_ROWA=1, tuning aid) read a's rows as they lie through a
+//   128-byte-swizzled [BM][BK] box -- no a^T launch, 0.5 GB less DRAM traffic
+//   at n = 8192 -- with 16-byte loads along k (8 per 4 k steps, the same count
+//   as the a^T slab) and rows ty + TY*i so a warp's loads hit distinct bank
+//   groups.  Bit-identical, but 13 % slower at every size.  Likely cause (from
+//   the SASS, not measured directly): more FFMA2s without a reused operand --
+//   1061 of 2048 against 810 for Mid, counting an instruction as slow when
+//   one bank parity is read three times.
 // * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage;
 //   thread 0 also issues the TMAs (a separate producer warp would push the
 //   block past the 2-blocks-per-SM register budget); the 8 compute warps
@@ -53,6 +69,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -63,7 +80,7 @@
 namespace pk {
 namespace {
 
-template <int TY_, int TX_, int BK_, int STAGES_, int MINB_, int AHEAD_>
+template <int TY_, int TX_, int BK_, int STAGES_, int MINB_, int AHEAD_, bool ROWA_ = false>
 struct Tile {
     static constexpr int TY = TY_, TX = TX_;              // compute threads, 8 x 8 outputs each
     static constexpr int BM = 8 * TY, BN = 8 * TX;        // block tile
@@ -73,6 +90,10 @@ struct Tile {
     static constexpr int NCOMP = TY * TX;
     static constexpr int NTHREADS = NCOMP;                // thread 0 also issues the TMAs
     static constexpr int MINB = MINB_;                    // resident CTAs per SM
+    // ROWA: a's rows as they lie ([BM rows][BK] box, 128-byte swizzle), no
+    // a^T launch; a thread's rows are ty + TY*i so the 16-byte a loads of a
+    // warp fall in distinct bank groups
+    static constexpr bool ROWA = ROWA_;
     static constexpr int A_SLAB = BK * BM * 4, B_SLAB = BK * BN * 4;
     static constexpr int STAGE_BYTES = A_SLAB + B_SLAB;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;  // ring + alignment + barriers
@@ -83,6 +104,13 @@ struct Tile {
 using Big = Tile<16, 16, 32, 3, 2, 1>;
 using Small = Tile<8, 8, 16, 3, 7, 1>;
 using Mid = Tile<16, 8, 32, 3, 3, 1>;
+using BigR = Tile<16, 16, 32, 3, 2, 1, true>;
+// one CTA per SM, 6 stages, 4 slabs ahead (PK_MM_TILE=big1, tuning aid): no
+// SM-mates to fall behind in the split phase, but 8 warps cover the ring less
+// well -- 0.80 / 0.85 / 0.86 of peak at n = 2048 / 4096 / 8192 (4-5 stages:
+// the same within 1 %)
+using Big1 = Tile<16, 16, 32, 6, 1, 4>;
+using MidR = Tile<16, 8, 32, 3, 3, 1, true>;
 
 // out[k][r] = a[r][k] for r < rows (row-major a with leading dimension lda)
 __global__ void __launch_bounds__(256) k_transpose_rows(const float *__restrict__ a, float *__restrict__ out,
@@ -177,7 +205,7 @@ template <class T>
 __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtensorMap *map_b, float *__restrict__ C,
                                         int64_t ldc, int64_t rlo, int m0, int n0, int kb, int ke, int &gs,
                                         unsigned char *smem, uint64_t *full, uint64_t *empty) {
-    constexpr int TX = T::TX, BM = T::BM, BN = T::BN, BK = T::BK, STAGES = T::STAGES, AHEAD = T::AHEAD;
+    constexpr int TX = T::TX, TY = T::TY, BM = T::BM, BN = T::BN, BK = T::BK, STAGES = T::STAGES, AHEAD = T::AHEAD;
     constexpr int STAGE_BYTES = T::STAGE_BYTES, A_SLAB = T::A_SLAB;
     const int tid = threadIdx.x;
     const int nk = ke - kb;
@@ -192,22 +220,27 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         fence_proxy_async();
         unsigned char *st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);
+        if (T::ROWA)
+            tma_load_2d(st, map_at, &full[s], (kb + j) * BK, m0);  // [BM rows][BK], 128-byte swizzle
+        else
+            tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);  // a^T slab [BK][BM]
         tma_load_2d(st + A_SLAB, map_b, &full[s], n0, (kb + j) * BK);
     };
     if (tid == 0)
         for (int j = 0; j < AHEAD && j < nk; j++) produce(j);
 
     const int tx = tid % TX, ty = tid / TX;
-    float *crow = C + (rlo + m0 + ty * 4) * ldc + n0 + tx * 4;
-    const int64_t chalf = (int64_t)(BM / 2) * ldc;
+    // this thread's 8 rows: ty*4 + {0..3} and BM/2 + ty*4 + {0..3} (a^T slab:
+    // two 16-byte loads per k step), or ty + TY*i (ROWA)
+    auto row_of = [&](int i) { return T::ROWA ? ty + TY * i : (i < 4 ? ty * 4 + i : BM / 2 + ty * 4 + i - 4); };
+    float *cbase = C + (rlo + m0) * ldc + n0 + tx * 4;
     // accumulators as packed column pairs: acc[i][jp] = {c[i][2jp], c[i][2jp+1]}
     // (the operand format of fma.rn.f32x2, so the loop never repacks them).
     // c through L2 (.cg): a tile's earlier slabs may have been run by another SM
     unsigned long long acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        const float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
+        const float *cr = cbase + row_of(i) * ldc;
         const ulonglong2 l = __ldcg(reinterpret_cast<const ulonglong2 *>(cr));
         const ulonglong2 h = __ldcg(reinterpret_cast<const ulonglong2 *>(cr + BN / 2));
         acc[i][0] = l.x; acc[i][1] = l.y; acc[i][2] = h.x; acc[i][3] = h.y;
@@ -216,22 +249,42 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
         const int g = gs + j, s = g % STAGES;
         if (tid == 0 && j + AHEAD < nk) produce(j + AHEAD);
         mbar_wait(&full[s], (g / STAGES) & 1);
-        const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM]
+        const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM] or [BM][BK]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
+        float4 a4[8];  // ROWA: a[row_of(i)][4q .. 4q+3]
 #pragma unroll
         for (int kk = 0; kk < BK; kk++) {
-            const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
-            const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
-            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            float af[8];
+            if (T::ROWA) {
+                static_assert(!T::ROWA || (BK == 32 && TY % 8 == 0), "ROWA: 128-byte rows, rows = ty mod 8");
+                if (kk % 4 == 0) {
+                    // 128-byte swizzle: the 16-byte chunk q of row r sits at chunk q ^ (r % 8);
+                    // r % 8 = ty % 8 for every row of this thread
+                    const unsigned char *ab = reinterpret_cast<const unsigned char *>(As) + ty * 128 +
+                                              (((kk / 4) ^ (ty & 7)) << 4);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) a4[i] = *reinterpret_cast<const float4 *>(ab + i * TY * 128);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    af[i] = kk % 4 == 0 ? a4[i].x : kk % 4 == 1 ? a4[i].y : kk % 4 == 2 ? a4[i].z : a4[i].w;
+            } else {
+                const float4 a0 = *reinterpret_cast<const float4 *>(As + kk * BM + ty * 4);
+                const float4 a1 = *reinterpret_cast<const float4 *>(As + kk * BM + BM / 2 + ty * 4);
+                af[0] = a0.x; af[1] = a0.y; af[2] = a0.z; af[3] = a0.w;
+                af[4] = a1.x; af[5] = a1.y; af[6] = a1.z; af[7] = a1.w;
+            }
             const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + tx * 4);
             const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(Bs + kk * BN + BN / 2 + tx * 4);
             const unsigned long long bp[4] = {b0.x, b0.y, b1.x, b1.y};
+            // b-pair-major: each b pair meets the 8 a values in a row, so the
+            // pair operand stays in the reuse cache and an FFMA2 reads at most
+            // two registers per bank (a-major issue: 0.858 of the FFMA peak
+            // for the bare loop, b-major 0.923 -- tools/ffma2_order_probe.cu)
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const unsigned long long ai = pack2(af[i], af[i]);
+            for (int jp = 0; jp < 4; jp++)
 #pragma unroll
-                for (int jp = 0; jp < 4; jp++) fma2p(acc[i][jp], ai, bp[jp]);
-            }
+                for (int i = 0; i < 8; i++) fma2p(acc[i][jp], pack2(af[i], af[i]), bp[jp]);
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
@@ -239,7 +292,7 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
     gs += nk;
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        float *cr = crow + (i < 4 ? i * ldc : chalf + (i - 4) * ldc);
+        float *cr = cbase + row_of(i) * ldc;
         *reinterpret_cast<ulonglong2 *>(cr) = make_ulonglong2(acc[i][0], acc[i][1]);
         *reinterpret_cast<ulonglong2 *>(cr + BN / 2) = make_ulonglong2(acc[i][2], acc[i][3]);
     }
@@ -289,6 +342,25 @@ __global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma(const __gri
 // before it has stored c (the tile's progress word equals its first slab),
 // and every item publishes its last slab after storing.  c is the fp32
 // accumulator between the parts, so the bits equal one launch.
+#ifdef PK_MM_TRACE
+// development trace (-DPK_MM_TRACE builds only): per CTA, globaltimer at the
+// start and at the end of every work item
+__device__ unsigned long long g_mm_trace[1024][32];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define MM_TRACE(slot) \
+    do { \
+        if (threadIdx.x == 0 && blockIdx.x < 1024 && (slot) < 32) g_mm_trace[blockIdx.x][slot] = gtime(); \
+    } while (0)
+#else
+#define MM_TRACE(slot) \
+    do { \
+    } while (0)
+#endif
+
 template <class T>
 __global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma_sched(const __grid_constant__ CUtensorMap map_at,
                                                                 const __grid_constant__ CUtensorMap map_b,
@@ -301,6 +373,8 @@ __global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma_sched(const
     __shared__ int next;
     unsigned char *smem;
     uint64_t *full, *empty;
+    int nt = 0;
+    MM_TRACE(nt++);
     mm_init<T>(smem, full, empty, smem_raw);
     int gs = 0;
     for (;;) {
@@ -312,6 +386,7 @@ __global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma_sched(const
         int m0, n0;
         tile_origin<T>(t, ntm, ntn, group, m0, n0);
         mm_item<T>(&map_at, &map_b, C, ldc, rlo, m0, n0, 0, ktiles, gs, smem, full, empty);
+        MM_TRACE(nt++);
     }
     for (int it = off[blockIdx.x]; it < off[blockIdx.x + 1]; it++) {
         const int3 w = items[it];
@@ -326,7 +401,9 @@ __global__ void __launch_bounds__(T::NTHREADS, T::MINB) k_matmul_tma_sched(const
             }
             __syncthreads();
         }
+        MM_TRACE(nt++);
         mm_item<T>(&map_at, &map_b, C, ldc, rlo, m0, n0, w.y, w.z, gs, smem, full, empty);
+        MM_TRACE(nt++);
         __syncthreads();  // every thread's c stores before the publication
         if (threadIdx.x == 0) {
             __threadfence();
@@ -465,14 +542,20 @@ int launch_tma_t(const float *a, const float *b, float *c, int64_t n, int64_t rl
     float *at = nullptr;
     int rc = PK_OK;
     CUtensorMap mat, mb;
-    cudaError_t e = scratch_alloc((void **)&at, (size_t)rows * K * sizeof(float), st);
-    if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul a^T workspace: %s", cudaGetErrorString(e));
-    if (rows % 64 == 0 && K % 64 == 0)
-        k_transpose_rows_v4<<<dim3((unsigned)(K / 64), (unsigned)(rows / 64)), 256, 0, st>>>(a + rlo * n, at, rows, n);
-    else
-        k_transpose_rows<<<dim3((unsigned)(K / 32), (unsigned)(rows / 32)), 256, 0, st>>>(a + rlo * n, at, rows, K, n);
-    rc = after_launch("matmul_transpose_a");
-    if (rc == PK_OK) rc = make_map(&mat, at, K, rows, rows, C::BM, C::BK);
+    if (C::ROWA) {
+        rc = make_map(&mat, a + rlo * n, rows, K, n, C::BK, C::BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+        cudaError_t e = scratch_alloc((void **)&at, (size_t)rows * K * sizeof(float), st);
+        if (e != cudaSuccess) return fail(PK_E_ALLOC, "matmul a^T workspace: %s", cudaGetErrorString(e));
+        if (rows % 64 == 0 && K % 64 == 0)
+            k_transpose_rows_v4<<<dim3((unsigned)(K / 64), (unsigned)(rows / 64)), 256, 0, st>>>(a + rlo * n, at,
+                                                                                                   rows, n);
+        else
+            k_transpose_rows<<<dim3((unsigned)(K / 32), (unsigned)(rows / 32)), 256, 0, st>>>(a + rlo * n, at, rows,
+                                                                                                K, n);
+        rc = after_launch("matmul_transpose_a");
+        if (rc == PK_OK) rc = make_map(&mat, at, K, rows, rows, C::BM, C::BK);
+    }
     if (rc == PK_OK) {
         if ((rc = make_map(&mb, b, K, Nc, n, C::BN, C::BK)) == PK_OK &&
             (rc = allow_smem((const void *)k_matmul_tma<C>, C::SMEM_BYTES)) == PK_OK &&
@@ -521,9 +604,22 @@ int launch_tma_t(const float *a, const float *b, float *c, int64_t n, int64_t rl
 
 int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64_t rlo, int64_t rhi, int64_t Nc,
                       int64_t K, int bm, int bn, cudaStream_t st) {
+    // PK_MM_ROWA=1 selects the row-major-a kernels (measured 13 % slower, kept
+    // as a tuning aid: see the ROWA note at the top of the file)
+    const char *renv = getenv("PK_MM_ROWA");
+    const bool rowa = renv && renv[0] == '1';
     if (bm == Small::BM && bn == Small::BN) return launch_tma_t<Small>(a, b, c, n, rlo, rhi, Nc, K, st);
-    if (bm == Mid::BM && bn == Mid::BN) return launch_tma_t<Mid>(a, b, c, n, rlo, rhi, Nc, K, st);
-    return launch_tma_t<Big>(a, b, c, n, rlo, rhi, Nc, K, st);
+    if (bm == Mid::BM && bn == Mid::BN)
+        return rowa ? launch_tma_t<MidR>(a, b, c, n, rlo, rhi, Nc, K, st) : launch_tma_t<Mid>(a, b, c, n, rlo, rhi, Nc, K, st);
+    const char *tenv = getenv("PK_MM_TILE");
+    if (tenv && !strcmp(tenv, "big1")) return launch_tma_t<Big1>(a, b, c, n, rlo, rhi, Nc, K, st);
+    return rowa ? launch_tma_t<BigR>(a, b, c, n, rlo, rhi, Nc, K, st) : launch_tma_t<Big>(a, b, c, n, rlo, rhi, Nc, K, st);
 }
 
 }  // namespace pk
+
+#ifdef PK_MM_TRACE
+extern "C" int pk_mm_trace(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, pk::g_mm_trace, sizeof(pk::g_mm_trace));
+}
+#endif

@@ -1,6 +1,7 @@
 """FP32 matmul TMA leaves at several n and at the 8-rank share of n = 8192
 (development probe): "big" = the 128 x 128 tile (B0 = 128, ub1*s = 128), "mid" =
-the 128 x 64 tile (ub1*s = 64).  Prints time, TFLOP/s and whether the bits of c
+the 128 x 64 tile (ub1*s = 64); a ":1" suffix selects the row-major-a kernels
+(PK_MM_ROWA=1) instead of the a^T-slab ones.  Prints time, TFLOP/s and whether the bits of c
 agree between the kernels (they must: same fma sequence).  PK_MM_KERNEL is set
 to the name for kernels the library selects by that knob (tuning aid).
 
@@ -29,6 +30,16 @@ for sz in sizes:
         L = binding.make_launch(kind, P, cases.select(kind, P).applied, _lib.DTYPE_F32, lo=0,
                                 hi=rows if share > 1 else 0)
         os.environ["PK_MM_KERNEL"] = k
+        # "big:1" / "mid:1": a's rows as they lie (PK_MM_ROWA=1); default: the a^T-slab kernels
+        # "big1": the 128 x 128 tile at one CTA per SM (PK_MM_TILE)
+        if k.startswith("big1"):
+            os.environ["PK_MM_TILE"] = k.split(":")[0]
+        else:
+            os.environ.pop("PK_MM_TILE", None)
+        if ":" in k:
+            os.environ["PK_MM_ROWA"] = k.split(":")[1]
+        else:
+            os.environ.pop("PK_MM_ROWA", None)
         c = c0.clone()
         _lib.launch(L, [a.data_ptr(), b.data_ptr(), c.data_ptr()], st.cuda_stream)
         torch.cuda.synchronize()
