@@ -80,7 +80,7 @@
 namespace pk {
 namespace {
 
-template <int TY_, int TX_, int BK_, int STAGES_, int MINB_, int AHEAD_, bool ROWA_ = false>
+template <int TY_, int TX_, int BK_, int STAGES_, int MINB_, int AHEAD_, bool ROWA_ = false, bool PWARP_ = false>
 struct Tile {
     static constexpr int TY = TY_, TX = TX_;              // compute threads, 8 x 8 outputs each
     static constexpr int BM = 8 * TY, BN = 8 * TX;        // block tile
@@ -88,7 +88,10 @@ struct Tile {
     static constexpr int STAGES = STAGES_;
     static constexpr int AHEAD = AHEAD_;                  // slabs in flight ahead of the one computed on
     static constexpr int NCOMP = TY * TX;
-    static constexpr int NTHREADS = NCOMP;                // thread 0 also issues the TMAs
+    // PWARP: one more warp only issues the TMAs (AHEAD = STAGES - 1 slabs in
+    // flight); otherwise thread 0 also issues them, AHEAD slabs ahead
+    static constexpr bool PWARP = PWARP_;
+    static constexpr int NTHREADS = NCOMP + (PWARP ? 32 : 0);
     static constexpr int MINB = MINB_;                    // resident CTAs per SM
     // ROWA: a's rows as they lie ([BM rows][BK] box, 128-byte swizzle), no
     // a^T launch; a thread's rows are ty + TY*i so the 16-byte a loads of a
@@ -105,11 +108,13 @@ using Big = Tile<16, 16, 32, 3, 2, 1>;
 using Small = Tile<8, 8, 16, 3, 7, 1>;
 using Mid = Tile<16, 8, 32, 3, 3, 1>;
 using BigR = Tile<16, 16, 32, 3, 2, 1, true>;
-// one CTA per SM, 6 stages, 4 slabs ahead (PK_MM_TILE=big1, tuning aid): no
-// SM-mates to fall behind in the split phase, but 8 warps cover the ring less
-// well -- 0.80 / 0.85 / 0.86 of peak at n = 2048 / 4096 / 8192 (4-5 stages:
-// the same within 1 %)
-using Big1 = Tile<16, 16, 32, 6, 1, 4>;
+// Big1P: 128 x 128 at one CTA per SM, 6 stages, a producer warp keeping 5
+// slabs in flight.  Used when the 128 x 128 tiles fill at most one wave of the
+// two-per-SM kernel (n = 2048: 256 tiles for 296 slots, no split possible):
+// 0.81 of peak against 0.72 (Big) and 0.80 (Mid); at n = 4096 / 8192 0.854 /
+// 0.867.  Thread 0 as producer instead (4 ahead): 0.80 / 0.847 / 0.861; a
+// producer warp for Mid (3 x 160 threads): no change.
+using Big1P = Tile<16, 16, 32, 6, 1, 5, false, true>;
 using MidR = Tile<16, 8, 32, 3, 3, 1, true>;
 
 // out[k][r] = a[r][k] for r < rows (row-major a with leading dimension lda)
@@ -226,8 +231,16 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
             tma_load_2d(st, map_at, &full[s], m0, (kb + j) * BK);  // a^T slab [BK][BM]
         tma_load_2d(st + A_SLAB, map_b, &full[s], n0, (kb + j) * BK);
     };
-    if (tid == 0)
+    if (T::PWARP) {
+        if (tid >= T::NCOMP) {  // the producer warp: one lane streams the item's slabs through the ring
+            if (tid == T::NCOMP)
+                for (int j = 0; j < nk; j++) produce(j);
+            gs += nk;
+            return;
+        }
+    } else if (tid == 0) {
         for (int j = 0; j < AHEAD && j < nk; j++) produce(j);
+    }
 
     const int tx = tid % TX, ty = tid / TX;
     // this thread's 8 rows: ty*4 + {0..3} and BM/2 + ty*4 + {0..3} (a^T slab:
@@ -247,7 +260,7 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
     }
     for (int j = 0; j < nk; j++) {
         const int g = gs + j, s = g % STAGES;
-        if (tid == 0 && j + AHEAD < nk) produce(j + AHEAD);
+        if (!T::PWARP && tid == 0 && j + AHEAD < nk) produce(j + AHEAD);
         mbar_wait(&full[s], (g / STAGES) & 1);
         const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM] or [BM][BK]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
@@ -611,8 +624,15 @@ int launch_matmul_tma(const float *a, const float *b, float *c, int64_t n, int64
     if (bm == Small::BM && bn == Small::BN) return launch_tma_t<Small>(a, b, c, n, rlo, rhi, Nc, K, st);
     if (bm == Mid::BM && bn == Mid::BN)
         return rowa ? launch_tma_t<MidR>(a, b, c, n, rlo, rhi, Nc, K, st) : launch_tma_t<Mid>(a, b, c, n, rlo, rhi, Nc, K, st);
+    // 128 x 128: one CTA per SM when the tiles fill at most one wave of the
+    // two-per-SM kernel (PK_MM_TILE=big / big1p forces either: tuning aid)
     const char *tenv = getenv("PK_MM_TILE");
-    if (tenv && !strcmp(tenv, "big1")) return launch_tma_t<Big1>(a, b, c, n, rlo, rhi, Nc, K, st);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((rhi - rlo) / Big::BM) * (Nc / Big::BN);
+    const bool one_wave = tenv ? !strcmp(tenv, "big1p") : tiles <= (int64_t)Big::MINB * sms;
+    if (!rowa && one_wave) return launch_tma_t<Big1P>(a, b, c, n, rlo, rhi, Nc, K, st);
     return rowa ? launch_tma_t<BigR>(a, b, c, n, rlo, rhi, Nc, K, st) : launch_tma_t<Big>(a, b, c, n, rlo, rhi, Nc, K, st);
 }
 

@@ -424,6 +424,38 @@ def test_matmul_mid_tile_split_bit_identical(cuda, rows):
     assert torch.equal(got[:lo], c.view(n, n)[:lo]) and torch.equal(got[hi:], c.view(n, n)[hi:])
 
 
+@pytest.mark.parametrize("n,rows", [(2048, (0, 2048)), (4096, (1024, 3072))])
+def test_matmul_tile_options_bit_identical(cuda, monkeypatch, n, rows):
+    """The 128 x 128 tile at one CTA per SM with a producer warp (Big1P, chosen
+    when the tiles fill one wave), at two CTAs per SM (Big), and the tiles that
+    read a's rows as they lie (PK_MM_ROWA=1): one ascending-k fma chain per
+    output, so the bits equal the 128 x 64 tile's on random fp32 data."""
+    torch = cuda
+    from paper_1801_04348_b200 import _lib, binding, programs
+
+    lo, hi = rows
+    g = torch.Generator(device="cuda").manual_seed(n)
+    a, b, c = (torch.rand(n * n, device="cuda", generator=g) * 2 - 1 for _ in range(3))
+    st = torch.cuda.current_stream().cuda_stream
+    ref = None
+    for env, ub1 in (({}, 4), ({"PK_MM_TILE": "big1p"}, 8), ({"PK_MM_TILE": "big"}, 8),
+                     ({"PK_MM_ROWA": "1"}, 8), ({"PK_MM_ROWA": "1"}, 4)):
+        for k in ("PK_MM_TILE", "PK_MM_ROWA"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        L = binding.make_launch(programs.original("matmul"), {"n": n, "B0": 128, "ub1": ub1, "s": 16}, (),
+                                _lib.DTYPE_F32, lo=lo, hi=hi)
+        got = c.clone()
+        _lib.launch(L, [a.data_ptr(), b.data_ptr(), got.data_ptr()], st)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = got
+        else:
+            assert torch.equal(got.view(torch.int32), ref.view(torch.int32)), env
+    assert torch.equal(ref[: lo * n], c[: lo * n]) and torch.equal(ref[hi * n:], c[hi * n:])
+
+
 @pytest.mark.parametrize("N,scale", [(32768, 1.0), (4099, 1e30), (777, 1e-30)])
 def test_matvec_float32_double_float_accumulation(cuda, N, scale):
     """float32 mat-vec at full size and at extreme magnitudes: the GPU's

@@ -12,7 +12,7 @@ import torch
 from paper_1801_04348_b200 import _lib, binding, cases, programs, run_program
 
 n = 8192
-P = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+P = {"n": n, "B0": 128, "ub1": 8, "s": int(sys.argv[1]) if len(sys.argv) > 1 else 16}
 rng = np.random.default_rng(0)
 a, b = (rng.random((n, n), dtype=np.float32) for _ in range(2))
 c = np.zeros((n, n), np.float32)

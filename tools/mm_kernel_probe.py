@@ -31,9 +31,10 @@ for sz in sizes:
                                 hi=rows if share > 1 else 0)
         os.environ["PK_MM_KERNEL"] = k
         # "big:1" / "mid:1": a's rows as they lie (PK_MM_ROWA=1); default: the a^T-slab kernels
-        # "big1": the 128 x 128 tile at one CTA per SM (PK_MM_TILE)
-        if k.startswith("big1"):
-            os.environ["PK_MM_TILE"] = k.split(":")[0]
+        # "big1p" / "big2": force the 128 x 128 tile at one / two CTAs per SM
+        # (PK_MM_TILE); plain "big" lets the library choose by the tile count
+        if k.startswith("big1p") or k.startswith("big2"):
+            os.environ["PK_MM_TILE"] = "big1p" if k.startswith("big1p") else "big"
         else:
             os.environ.pop("PK_MM_TILE", None)
         if ":" in k:
