@@ -86,7 +86,13 @@ def main():
                     lines.append("| %s | %s %s |" % (k, v, u))
         lines.append("")
     os.makedirs("profiles", exist_ok=True)
-    traffic = {}
+    # records of kernels not captured this time stay (each carries its round)
+    tpath = os.path.join("profiles", "ncu_traffic.json")
+    try:
+        with open(tpath) as fh:
+            traffic = json.load(fh)
+    except (OSError, ValueError):
+        traffic = {}
     for name, path in reps:
         for kern in summary(path):
             rd, wr = kern.get("dram__bytes_read.sum"), kern.get("dram__bytes_write.sum")
@@ -96,7 +102,7 @@ def main():
                                  "dram_bytes": to_bytes(*rd) + to_bytes(*wr),
                                  "gpu_time_us": to_us(*t) if t else None,
                                  "report": os.path.basename(path), "round": rnd}
-    with open(os.path.join("profiles", "ncu_traffic.json"), "w") as fh:
+    with open(tpath, "w") as fh:
         json.dump(traffic, fh, indent=1, sort_keys=True)
         fh.write("\n")
     out = os.path.join("profiles", "%s_ncu.md" % rnd)
