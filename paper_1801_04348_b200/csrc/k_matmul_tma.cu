@@ -219,6 +219,21 @@ __device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, 
     n0 = ((g & 1) ? ntn - 1 - col : col) * C::BN;
 }
 
+// mbarrier wait with a suspend-time hint (ns): the thread sleeps in the
+// barrier instead of re-polling.  For the producer warp's empty-stage waits
+// (paired A/B on one B200: Big1P at n = 2048 0.820 -> 0.835 of peak at 1 us,
+// same at 0.5 / 2 us); the thread-0 producers of the other tiles poll (the
+// hint cost Mid 1.6 % at n = 8192), and so do the consumers (no gain).
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+            : "memory");
+}
+
 // Slabs [kb, ke) of tile (m0, n0): c rows -> packed accumulators, the ring,
 // accumulators -> c.  gs: this CTA's running slab count (the ring's stage and
 // barrier phase continue across work items).
@@ -234,7 +249,10 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
     // slab j + AHEAD once every warp has released that stage's previous slab
     auto produce = [&](int j) {
         const int g = gs + j, s = g % STAGES;
-        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        if (T::PWARP)
+            mbar_wait_hint(&empty[s], ((g / STAGES) & 1) ^ 1, 1000);
+        else
+            mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
         // the consumers read the stage through the generic proxy (LDS); order
         // those reads before the async-proxy (TMA) overwrite -- without this
         // fence n = 8192 runs lost a k-slab of one tile every few launches
