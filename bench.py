@@ -673,13 +673,14 @@ def bench_kernels(peaks, mv, no_tune: bool = False, cpu: bool = True) -> dict:
         gen.manual_seed(0x1801)
         bufs = _fill(fam, shapes, gen)
         ptrs = [x.data_ptr() for x in bufs]
-        # tune (B, s) / (B0, B1, s) inside the live case on 2 time steps, run the full T
-        tune_base = dict(params, T=2) if "T" in params else dict(params)
+        # tune (B, s) / (B0, B1, s) inside the live case on 4 time steps, run the full T
+        # (2 steps x 2 launches picked a 6 % slower 1-D leaf on one box: too short to time)
+        tune_base = dict(params, T=4) if "T" in params else dict(params)
         if no_tune:
             tuned, trials = dict(tune_base, **TUNE_GRIDS[fam][0]), []
         else:
-            tuned, trials = autotune.autotune(kind, tune_base, machine=mv, buffers=bufs, reps=2,
-                                              grid=TUNE_GRIDS.get(fam))
+            tuned, trials = autotune.autotune(kind, tune_base, machine=mv, buffers=bufs,
+                                              reps=4 if "T" in params else 2, grid=TUNE_GRIDS.get(fam))
         run_params = dict(tuned, T=params["T"]) if "T" in params else tuned
         sel = cases.select(kind, run_params, mv)
         L = binding.make_launch(kind, run_params, sel.applied, _lib.DTYPE_I32)
