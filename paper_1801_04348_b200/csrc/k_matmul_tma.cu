@@ -103,10 +103,16 @@ struct Tile {
 };
 // BK = 32, 3 stages, 1 slab ahead for the two-per-SM tile (measured best, see
 // above); the small tile keeps 3 stages of 16-deep slabs (24 KB a CTA, 7 CTAs
-// in 227 KB); Mid: 128 x 64 on 128 threads, 3 CTAs per SM (72 KB rings).
+// in 227 KB); Mid: 128 x 64 on 128 compute threads + a producer warp, 3 CTAs
+// per SM (72 KB rings).
 using Big = Tile<16, 16, 32, 3, 2, 1>;
 using Small = Tile<8, 8, 16, 3, 7, 1>;
-using Mid = Tile<16, 8, 32, 3, 3, 1>;
+// Mid: the 128 x 64 tile, 3 CTAs of 4 compute warps + 1 producer warp per SM
+// (the producer sleeps in the empty-stage barrier, mbar_wait_hint): 0.872 ->
+// 0.891 of peak at n = 8192 and 0.804 -> 0.826 at n = 2048 against thread 0
+// as producer (paired runs on one box; without the sleep the producer warp
+// gained nothing)
+using Mid = Tile<16, 8, 32, 3, 3, 2, false, true>;
 using BigR = Tile<16, 16, 32, 3, 2, 1, true>;
 // Big1P: 128 x 128 at one CTA per SM, 6 stages, a producer warp keeping 5
 // slabs in flight.  Used when the 128 x 128 tiles fill at most one wave of the
