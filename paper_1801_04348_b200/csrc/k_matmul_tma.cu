@@ -228,8 +228,8 @@ __device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, 
 // mbarrier wait with a suspend-time hint (ns): the thread sleeps in the
 // barrier instead of re-polling.  For the producer warp's empty-stage waits
 // (paired A/B on one B200: Big1P at n = 2048 0.820 -> 0.835 of peak at 1 us,
-// same at 0.5 / 2 us); the thread-0 producers of the other tiles poll (the
-// hint cost Mid 1.6 % at n = 8192), and so do the consumers (no gain).
+// same at 0.5 / 2 us); a thread-0 producer polls (the hint cost the 128 x 64
+// tile 1.6 % at n = 8192 before it had a producer warp).
 __device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
     uint32_t ok = 0;
     while (!ok)
@@ -301,7 +301,13 @@ __device__ __forceinline__ void mm_item(const CUtensorMap *map_at, const CUtenso
     for (int j = 0; j < nk; j++) {
         const int g = gs + j, s = g % STAGES;
         if (!T::PWARP && tid == 0 && j + AHEAD < nk) produce(j + AHEAD);
-        mbar_wait(&full[s], (g / STAGES) & 1);
+        // with a producer warp, a consumer that runs ahead sleeps in the barrier
+        // instead of polling (paired A/B: 128 x 64 at n = 8192 0.880 -> 0.891 at
+        // 200 ns or 1 us; n = 2048 -0.6 %, where the tuner picks Big1P)
+        if (T::PWARP)
+            mbar_wait_hint(&full[s], (g / STAGES) & 1, 200);
+        else
+            mbar_wait(&full[s], (g / STAGES) & 1);
         const float *As = reinterpret_cast<const float *>(smem + s * STAGE_BYTES);  // [BK][BM] or [BM][BK]
         const float *Bs = As + BK * BM;                                               // [BK][BN]
         float4 a4[8];  // ROWA: a[row_of(i)][4q .. 4q+3]
