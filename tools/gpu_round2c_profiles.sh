@@ -2,7 +2,7 @@
 # Round-2c evidence after the b-pair-major FFMA2 order and the Big1P tile:
 # launch list of the bench command + one ncu --set full capture per FP32
 # matmul leaf the tuners pick (numbers under ncu are evidence, never bench values).
-D=gpurun_out/${OUT:-r02dprof}
+D=gpurun_out/${OUT:-r02eprof}
 mkdir -p $D
 ncu --metrics gpu__time_duration.sum --clock-control none -c 5000 --csv --log-file $D/launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-tune > $D/bench_under_ncu.log 2>&1
