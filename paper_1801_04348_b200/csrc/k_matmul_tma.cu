@@ -10,30 +10,23 @@
 //   scalar shared loads per k step -- saves the transpose launch and 0.5 GB
 //   of DRAM traffic but measured 12 % slower: 19.3 vs 17.0 ms at n = 8192,
 //   the extra loads spill at the 128-register budget.)
-// * Three tiles (template Tile), same thread mapping (8 x 8 outputs per
-//   thread) and numerics: 128 x 128 on 256 threads, 2 CTAs per SM, for the
-//   large matrices; 128 x 64 on 128 threads, 3 CTAs per SM, for n = 2048;
-//   64 x 64 on 64 threads (16-deep slabs, up to 8 CTAs per SM), which the
-//   tuner picks for small ones (n = 1024: 64 tiles of 128 x 128 leave most SMs
-//   idle; 34.7 against 31.9 TFLOP/s for the best other leaf).
-// * Why 128 x 64 at n = 2048.  The exact result forbids splitting a tile's
-//   reduction except in k order, so a tile's KS slabs run in sequence at one
-//   CTA's speed (1/c of an SM with c CTAs per SM); the order-preserving split
-//   below balances the SMs only when every run is at least one tile long, i.e.
-//   when there are at least 148 c tiles.  128 x 128 has 256 tiles for 296
-//   slots (0.865 balance at best); 128 x 64 has 512 for 444: split into equal
-//   runs of 1.15 tiles -> 57.2 against 51.8 TFLOP/s (tools/mm_kernel_probe.py).
-//   Measured and dropped: one CTA per SM with the whole register file
-//   (54.2 at n = 2048, 0.76 of peak at n = 8192: 8 warps do not cover the ring's
-//   waits); 256 x 128 on 512 threads (= Big at 2048, 0.860 at 8192); a's rows
-//   loaded as they lie through a 128-byte-swizzled box (no transpose launch) at
-//   255 / 170 registers: 10 % slower than the a^T slab at every size; 8 x 16
-//   outputs per thread (128 threads, 200 registers, 2 CTAs per SM): 0.830 of
-//   peak at n = 8192 against 0.876, although its bare loop is 2 % faster;
-//   8 x 4 per thread (more warps for small n: 128 x 64 on 256 threads, 64 x 64
-//   on 128) 38.6 / 36.0 TFLOP/s at n = 1024 against 38.4 for the 128 x 64 tile
-//   -- n = 1024 has 2^20 outputs, 4 warps of 8 x 8 per SM: the few warps, not
-//   the blocking, set its rate.
+// * Tiles (template Tile), same thread mapping (8 x 8 outputs per thread) and
+//   numerics: 128 x 64 on 128 compute threads + a producer warp, 3 CTAs per SM
+//   (the tuner's pick at n = 8192 and n = 1024); 128 x 128 on 256 threads, 2
+//   CTAs per SM (thread 0 issues the TMAs; the best for an 8-rank share);
+//   128 x 128 at one CTA per SM with a producer warp (Big1P), which the
+//   launcher takes when the 128 x 128 tiles fill one wave (n = 2048); 64 x 64
+//   on 64 threads (16-deep slabs, up to 7 CTAs per SM) for small matrices.
+// * Small grids.  The exact result forbids splitting a tile's reduction except
+//   in k order, so a tile's KS slabs run in sequence at one CTA's speed (1/c of
+//   an SM with c CTAs per SM); the order-preserving split below balances the
+//   SMs only when every run is at least one tile long, i.e. with at least
+//   148 c tiles.  n = 2048: 128 x 128 has 256 tiles for 296 two-per-SM slots
+//   (0.865 balance at best), hence Big1P (256 tiles for 148 CTAs: runs of 1.73
+//   tiles).  Measured and dropped (tools/mm_kernel_probe.py; DESIGN.md section
+//   7 lists the numbers): 256 x 128 on 512 threads; 8 x 16 and 8 x 4 outputs
+//   per thread; BK = 16 rings; pacing the CTAs of an SM in the split phase;
+//   transposing a inside the kernel or beside it.
 // * Issue order of the FFMA2s.  An FFMA2 with a scalar a, a b pair and a c pair
 //   reads up to 5 registers; when neither the a nor the b operand carries over
 //   from the previous instruction (operand reuse cache) one register bank is
@@ -54,18 +47,17 @@
 //   the SASS, not measured directly): more FFMA2s without a reused operand --
 //   1061 of 2048 against 810 for Mid, counting an instruction as slow when
 //   one bank parity is read three times.
-// * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage;
-//   thread 0 also issues the TMAs (a separate producer warp would push the
-//   block past the 2-blocks-per-SM register budget); the 8 compute warps
-//   wait on "full", run BK x 64 FFMAs per thread from 128-bit shared loads,
-//   and release the stage with one arrive per warp on "empty" -- no
-//   block-wide barrier in the main loop, no register staging or shared
-//   stores.
-// * BK = 32, 3 stages, 1 slab in flight ahead (measured on B200, n = 8192:
-//   66.1 TFLOP/s against 65.0 for BK = 16 / 4 stages / 3 ahead): the refill
-//   of a stage then waits on the slab released two k-steps earlier, so
-//   thread 0's warp never waits for the slowest warp of the current step,
-//   and the wider slab halves the barrier round trips per FLOP.
+// * STAGES-deep ring of slabs, one full/empty mbarrier pair per stage; the
+//   compute warps wait on "full", run BK x 64 FFMAs per thread from 128-bit
+//   shared loads, and release the stage with one arrive per warp on "empty"
+//   -- no block-wide barrier in the main loop, no register staging or shared
+//   stores.  The TMAs come from a producer warp where the register budget
+//   allows one (its waits, and the consumers', sleep in the barrier:
+//   mbar_wait_hint), else from thread 0, one slab ahead.
+// * BK = 32, 3 stages (measured on B200, n = 8192: 66.1 TFLOP/s against 65.0
+//   for BK = 16 / 4 stages / 3 ahead on the 128 x 128 tile; 16-deep slabs
+//   lost 4-5 % on 128 x 64 too): the wider slab halves the barrier round
+//   trips per FLOP.
 #include <cuda.h>
 
 #include <cstdlib>
