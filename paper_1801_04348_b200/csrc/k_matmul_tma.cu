@@ -217,21 +217,6 @@ __device__ __forceinline__ void tile_origin(int t, int ntm, int ntn, int group, 
     n0 = ((g & 1) ? ntn - 1 - col : col) * C::BN;
 }
 
-// mbarrier wait with a suspend-time hint (ns): the thread sleeps in the
-// barrier instead of re-polling.  For the producer warp's empty-stage waits
-// (paired A/B on one B200: Big1P at n = 2048 0.820 -> 0.835 of peak at 1 us,
-// same at 0.5 / 2 us); a thread-0 producer polls (the hint cost the 128 x 64
-// tile 1.6 % at n = 8192 before it had a producer warp).
-__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
-    uint32_t ok = 0;
-    while (!ok)
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
-            : "memory");
-}
-
 // Slabs [kb, ke) of tile (m0, n0): c rows -> packed accumulators, the ring,
 // accumulators -> c.  gs: this CTA's running slab count (the ring's stage and
 // barrier phase continue across work items).
