@@ -148,13 +148,13 @@ def test_transpose_full_size_property(cuda):
     assert torch.equal(out["c"].reshape(N, N).view(torch.int32), a.t().view(torch.int32))
 
 
-def _fp32_matmul_full_size(torch, tf32x3: bool):
+def _fp32_matmul_full_size(torch, tf32x3: bool, s: int = 16):
     from paper_1801_04348_b200 import last_run, programs
 
     n = 8192
     g = torch.Generator(device="cuda").manual_seed(0x1801)
     a, b, c = (torch.rand((n, n), device="cuda", generator=g) * 2 - 1 for _ in range(3))
-    params = {"n": n, "B0": 128, "ub1": 8, "s": 16}
+    params = {"n": n, "B0": 128, "ub1": 8, "s": s}
     got = _run(programs.source("matmul"), params, {"a": a, "b": b, "c": c}, tf32x3=tf32x3)["c"]
     assert last_run().launch["dtype"] == "f32"
     want = c.double() + a.double() @ b.double()  # binary64 reference (the interpreter sums binary64)
@@ -163,10 +163,13 @@ def _fp32_matmul_full_size(torch, tf32x3: bool):
     return err
 
 
-def test_matmul_fp32_full_size_tolerance(cuda):
+@pytest.mark.parametrize("s", [16, 8])
+def test_matmul_fp32_full_size_tolerance(cuda, s):
     """BASELINE configs[1] headline at its size: n = 8192 on U[-1,1) against a
-    binary64 product, normalised error <= 1e-5 * K / 1024 (north_star)."""
-    err = _fp32_matmul_full_size(cuda, False)
+    binary64 product, normalised error <= 1e-5 * K / 1024 (north_star), on
+    the 128 x 128 tile (s = 16) and the 128 x 64 producer-warp tile the
+    bench's tuner picks (s = 8)."""
+    err = _fp32_matmul_full_size(cuda, False, s)
     assert err <= _matmul_tol(8192), err
 
 
@@ -273,7 +276,8 @@ def test_matmul_tf32x3_tcgen05_within_tolerance(cuda, oracle_mod):
 # ---- BASELINE-size parity through properties that do not need the CPU oracle ----
 
 
-def test_matmul_full_size_integer_valued_exact(cuda):
+@pytest.mark.parametrize("s", [16, 8])
+def test_matmul_full_size_integer_valued_exact(cuda, s):
     """n = 8192 (BASELINE configs[1]) on the tuned TMA tile: integer-valued fp32
     in [-8, 8] keeps every partial sum an integer below 2^24, so the result
     must equal an exact binary64 product (torch float64 on the GPU)."""
@@ -289,7 +293,7 @@ def test_matmul_full_size_integer_valued_exact(cuda):
     # several launches: a missing proxy fence between the consumers' shared
     # loads and the next TMA refill once corrupted one tile every few runs
     for rep in range(4):
-        got = _run(programs.source("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": 16},
+        got = _run(programs.source("matmul"), {"n": n, "B0": 128, "ub1": 8, "s": s},
                    {"a": a, "b": b, "c": c})["c"]
         assert last_run().applied == ()
         assert torch.equal(got.reshape(n, n).double(), want), rep
