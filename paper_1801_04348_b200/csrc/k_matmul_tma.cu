@@ -642,11 +642,12 @@ int launch_tma_t(const float *a, const float *b, float *c, int64_t n, int64_t rl
         cfg.numAttrs = pdl ? 1 : 0;
         cudaError_t e;
         if (split) {
-            if (!pdl) cudaMemsetAsync(progress, 0, (size_t)(T + 1) * sizeof(int), st);
+            e = pdl ? cudaSuccess : cudaMemsetAsync(progress, 0, (size_t)(T + 1) * sizeof(int), st);
             cfg.gridDim = dim3((unsigned)P);
-            e = cudaLaunchKernelEx(&cfg, k_matmul_tma_sched<C>, mat, mb, c, n, rlo, ntm, ntn, group,
-                                   (int)schedule_base(T, (int)P), (int)KS, (const int3 *)d.items, (const int *)d.off,
-                                   progress, progress + T);
+            if (e == cudaSuccess)
+                e = cudaLaunchKernelEx(&cfg, k_matmul_tma_sched<C>, mat, mb, c, n, rlo, ntm, ntn, group,
+                                       (int)schedule_base(T, (int)P), (int)KS, (const int3 *)d.items,
+                                       (const int *)d.off, progress, progress + T);
         } else {
             cfg.gridDim = dim3((unsigned)T);
             e = cudaLaunchKernelEx(&cfg, k_matmul_tma<C>, mat, mb, c, n, rlo, ntn, (int)KS, group);
