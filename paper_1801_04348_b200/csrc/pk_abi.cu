@@ -399,11 +399,16 @@ int pk_jacobi_narrow(const pk_launch_t *L, const void *a, int32_t *narrow, void 
 
 namespace {
 
+// Pipeline cut of pk_run_host (build options).  n = 8192 FP32 matmul e2e
+// with the 128 x 64 producer-warp leaf: 8 x 4 22.1 ms, 12 x 4 21.1, 16 x 4
+// 21.4, 12 x 6 20.85, 14 x 6 20.83, 16 x 6 20.93, 12 x 8 22.8 (chunks are
+// whole 128-row multiples: 12 requested = 11 of 768 rows).  Finer uploads
+// give the first chunks work sooner (tools/e2e_pipeline_model.py).
 #ifndef PK_RH_CHUNKS
-#define PK_RH_CHUNKS 8
+#define PK_RH_CHUNKS 12
 #endif
 #ifndef PK_RH_SLICES
-#define PK_RH_SLICES 4
+#define PK_RH_SLICES 6
 #endif
 constexpr int kMaxChunks = PK_RH_CHUNKS;                  // pipeline depth limit of pk_run_host
 constexpr int kMaxDevices = 64;                // pk_launch_multi

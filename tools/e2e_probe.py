@@ -7,7 +7,7 @@ if len(sys.argv) > 1:
 import time, torch, numpy as np
 from paper_1801_04348_b200 import binding, cases, programs
 n=8192
-kind=programs.original("matmul"); P={"n":n,"B0":128,"ub1":8,"s":16}
+kind=programs.original("matmul"); P={"n":n,"B0":128,"ub1":8,"s":int(sys.argv[2]) if len(sys.argv)>2 else 8}
 sel=cases.select(kind,P,"live")
 L=binding.make_launch(kind,P,sel.applied,_lib.DTYPE_F32)
 hs=[torch.rand(n*n).pin_memory() for _ in range(3)]
