@@ -479,8 +479,9 @@ def main() -> int:
             "tensor_tflops": round(3 * tf, 1),
             # dense TF32 is half the BF16 rate on B200 (1.1 vs 2.25 PFLOP/s nominal): the
             # measured BF16 burst / 2 is the measured-TF32 ceiling; the nominal one beside it
-            "frac_of_tf32_dense": round(3 * tf / (peaks.get("bf16_tflops", 2250.0) / 2), 4),
-            "frac_of_tf32_nominal": round(3 * tf / (sm_count * 4096 * peaks["sm_max_mhz"] * 1e-6), 4),
+            # (per GPU: the value is the whole job's, over `world` GPUs)
+            "frac_of_tf32_dense": round(3 * tf / world / (peaks.get("bf16_tflops", 2250.0) / 2), 4),
+            "frac_of_tf32_nominal": round(3 * tf / world / (sm_count * 4096 * peaks["sm_max_mhz"] * 1e-6), 4),
             "note": "3xTF32 split (hi*hi + hi*lo + lo*hi) on tcgen05 kind::tf32, fp32 TMEM accumulation; "
                     "within the FP32 tolerance, not the FFMA path's rounding sequence"}
     except (NotImplementedError, ValueError, RuntimeError) as exc:  # shapes the variant does not tile
