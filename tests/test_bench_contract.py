@@ -33,3 +33,22 @@ def test_reference_arm_prints_one_contract_line():
 def test_reference_arm_other_ranks_exit_quietly():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     assert _run("--steps", "1", "--warmup", "0", "--gpus", "2", env=env) == []
+
+
+def test_committed_ncu_traffic_covers_every_measured_kernel():
+    """roofline.traffic and each family's traffic come from profiles/ncu_traffic.json
+    under the keys bench.py looks up (a renamed capture would silently drop them)."""
+    sys.path.insert(0, REPO)
+    import bench
+
+    with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+        recs = json.load(fh)
+    for fam, key in bench.TRAFFIC_KEYS.items():
+        assert key in recs, (fam, key)
+    for n in (2048, 8192):
+        for s in (8, 16):
+            key = bench.matmul_traffic_key(n, {"B0": 128, "ub1": 8, "s": s})
+            assert key in recs, key
+    assert bench.matmul_traffic_key(1024, {"B0": 128, "ub1": 8, "s": 16}) is None
+    for rec in recs.values():
+        assert rec["dram_bytes"] > 0 and rec["kernel"] and rec["round"]
