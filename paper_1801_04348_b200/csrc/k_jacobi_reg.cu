@@ -251,7 +251,13 @@ __global__ void __launch_bounds__(kJ1Threads) k_jacobi1d_reg(const int *__restri
 // alignment: on an 8-byte row the thread loads the aligned quad c+2..c+5 and
 // takes c..c+1 (and c-1) from the previous lane.  Bands start on odd rows so
 // the loaded rows' phases are the same in every band.
-constexpr int kJ2Warps = 4, kJ2R = 4;
+// Output rows per band (build option): a block loads R + 2 rows for R.
+// 16386^2, T = 10: R = 4 6.45 TB/s, 6 6.27, 8 6.07, 12 5.66 (more registers,
+// fewer blocks per SM) -- the halo rows come from L2 (DRAM bytes 0.98x).
+#ifndef PK_J2R
+#define PK_J2R 4
+#endif
+constexpr int kJ2Warps = 4, kJ2R = PK_J2R;
 
 struct RowQ {
     int4 q;  // row[c .. c+3]
